@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Benchmark: cuSZ-Hi compress + decompress round trip on B200.
+
+Workload (BASELINE.json configs[1]): Nyx-shape 512^3 f32 synthetic Gaussian
+random field (SURVEY §8d "GRF-k"), rel-eb 1e-3, CR pipeline.  One step = one
+compress (resolve eb -> tune -> predict/quantize/reorder -> Huffman/RRE4/
+TCMS8/RZE1 -> archive, incl. the size read-back) plus one decompress of that
+archive.  `value` = input bytes of all ranks / (compress + decompress time),
+device-resident buffers; compress_gbs / decompress_gbs are the two halves.
+
+N > 1 (torchrun): weak scaling over independent axis-0 slabs -- every rank
+compresses its own 512^3 slab of a (512N)x512x512 volume; the only exchange is
+an all-gather of the per-slab archive sizes (NCCL) that assembles the slab
+container offsets.  Timing: CUDA events on the stream the library
+launches on, barrier + synchronize on both sides, max over ranks.
+
+--impl reference: the CPU oracle (C restatement of the reference path,
+oracle/; `kind: port`) on the same workload with all host threads, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="cr", choices=["cr", "tp"])
+    ap.add_argument("--kind", default="grf", choices=["grf", "gauss", "rough"])
+    ap.add_argument("--size", type=int, default=512)
+    ap.add_argument("--eb", type=float, default=1e-3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+METRIC = "compress+decompress round-trip GB/s (input bytes / (t_compress + t_decompress)), rel-eb 1e-3"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# algorithmic bytes per launch for the kernels we attribute a roofline to
+def algo_bytes(phase: str, n: int, prec: int, archive: int) -> float:
+    if phase == "level1":  # 7/8 targets: read orig, read f64 2-lattice, write code bytes
+        return n * (7 / 8 * prec + 1 / 8 * 8 + 7 / 8)
+    if phase == "rlevel1":  # read codes + f64 2-lattice, write all outputs
+        return n * (7 / 8 + 1 / 8 * 8 + prec)
+    if phase == "eb_range":
+        return n * prec
+    if phase in ("huff_encode",):
+        return n
+    if phase in ("decode_stream",):
+        return n + archive
+    return 0.0
+
+
+def run_reference(args):
+    from oracle import oracle
+    from paper_2507_11165_b200 import synth
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    oracle.set_threads(cores)
+    S = args.size
+    vals = synth.make("grf", (S, S, S), seed=2025) if args.kind == "grf" else synth.make(args.kind, (S, S, S), seed=2025)
+    n = vals.size
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        blob = oracle.compress(vals, "rel", args.eb, args.mode, 3)
+        out, _ = oracle.decompress(blob)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    t = sum(times)
+    v = n * 4 * args.steps / t / 1e9
+    line = {
+        "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32->u8 codes (f64 predictor)", "data": "synthetic",
+        "config": {"workload": f"{args.kind} {S}^3 f32 rel-eb {args.eb} {args.mode.upper()}",
+                   "l2": "input 537 MB > 126 MB L2"},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"full {S}^3 workload, oracle/hb_oracle.c (OpenMP, {cores} threads)"},
+        "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cr": round(n * 4 / len(blob), 3),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(vals_host, args):
+    from oracle import oracle
+    cores = os.cpu_count() or 1
+    oracle.set_threads(cores)
+    # bounded sample: leading axis-0 planes of the same field (~10-30 s of CPU work)
+    planes = min(vals_host.shape[0], 128)
+    sample = np.ascontiguousarray(vals_host[:planes])
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        blob = oracle.compress(sample, "rel", args.eb, args.mode, 3)
+        oracle.decompress(blob)
+        reps += 1
+        if time.perf_counter() - t0 > 10.0 or reps >= 5:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(sample.nbytes * reps / dt / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"{planes}x{vals_host.shape[1]}x{vals_host.shape[2]} leading slab of the same field, "
+                      f"{reps} round trips, oracle/hb_oracle.c OpenMP"}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2507_11165_b200 as hb
+    from paper_2507_11165_b200 import _lib, synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    S = args.size
+    vals = synth.make_device(args.kind, (S, S, S), seed=2025 + rank)
+    f = hb.Field(vals)
+    spec = hb.ErrorBoundSpec("rel", args.eb)
+    n = f.count
+    nbytes = n * 4
+    stream = torch.cuda.current_stream()
+
+    out_buf = torch.empty(hb.compress_bound(f.dims, 4), dtype=torch.uint8, device="cuda")
+    rec_buf = torch.empty_like(vals)
+
+    def step():
+        a = hb.compress_device(f, spec, args.mode, out=out_buf)
+        hb.decompress_device(a, f.dims, np.float32, out=rec_buf)
+        return a
+
+    for _ in range(args.warmup):
+        arch = step()
+    # correctness guard on the timed configuration
+    err = (rec_buf.double() - vals.double()).abs().max().item()
+    info = hb.section_sizes(arch.cpu().numpy().tobytes())
+    assert err <= info["abs_eb"], (err, info["abs_eb"])
+    archive_len = arch.numel()
+
+    _lib.set_profile(True)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    phases = {}
+    launches = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for k in range(args.steps):
+            ev[k][0].record(stream)
+            a = hb.compress_device(f, spec, args.mode, out=out_buf)
+            launches += _lib.last_launch_count()
+            for nm, ms in _lib.last_phases():
+                phases.setdefault(nm, []).append(ms)
+            ev[k][1].record(stream)
+            if world > 1:  # slab container: all-gather of archive sizes
+                sz = torch.tensor([a.numel()], dtype=torch.int64, device="cuda")
+                allsz = torch.empty(world, dtype=torch.int64, device="cuda")
+                dist.all_gather_into_tensor(allsz, sz)
+            hb.decompress_device(a, f.dims, np.float32, out=rec_buf)
+            launches += _lib.last_launch_count()
+            for nm, ms in _lib.last_phases():
+                phases.setdefault(nm, []).append(ms)
+            ev[k][2].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    _lib.set_profile(False)
+    tc = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3
+    td = sum(e[1].elapsed_time(e[2]) for e in ev) / 1e3
+    t = torch.tensor([tc + td, tc, td], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ttot, tcm, tdm = t.tolist()
+    total_bytes = nbytes * world * args.steps
+    value = total_bytes / ttot / 1e9
+
+    # roofline of the dominant kernel (CUDA events around it on the launch stream)
+    peak, peak_kind = peaks()
+    cand = {k: statistics.mean(v) for k, v in phases.items() if algo_bytes(k, n, 4, archive_len) > 0}
+    dom = max(cand, key=cand.get) if cand else None
+    roof = None
+    if dom:
+        ms = cand[dom]
+        ab = algo_bytes(dom, n, 4, archive_len)
+        ach = ab / (ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 2), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": None, "algo_bytes": int(ab), "ms": round(ms, 4),
+                "peak_kind": peak_kind}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * ttot / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32->u8 codes (f64 predictor)",
+        "data": "synthetic (GPU-generated GRF-k, SURVEY 8d)",
+        "config": {"workload": f"{args.kind} {S}^3 f32 per GPU, rel-eb {args.eb}, {args.mode.upper()} pipeline",
+                   "parallelism": f"axis-0 slabs x{world}" if world > 1 else "single GPU",
+                   "l2": "input 537 MB > 126 MB L2, no flush needed"},
+        "compress_gbs": round(total_bytes / tcm / 1e9, 3), "decompress_gbs": round(total_bytes / tdm / 1e9, 3),
+        "cr": round(nbytes / archive_len, 3), "archive_bytes": archive_len,
+        "gpu_launches": launches,
+        "roofline": roof,
+        "phases_ms": {k: round(statistics.mean(v), 4) for k, v in phases.items()},
+        "clocks": clk.summary(),
+    }
+
+    # end-to-end through the reference-facing API with host (pinned) buffers
+    if not args.no_e2e:
+        host_in = torch.empty((S, S, S), dtype=torch.float32, pin_memory=True)
+        host_in.copy_(vals)
+        host_out = torch.empty((S, S, S), dtype=torch.float32, pin_memory=True)
+        fh = hb.Field(host_in.numpy())
+        blob = None
+        for _ in range(1):
+            blob = hb.compress(fh, spec, args.mode)
+            hb.decompress(blob, out=host_out.numpy())
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            blob = hb.compress(fh, spec, args.mode)
+            hb.decompress(blob, out=host_out.numpy())
+        torch.cuda.synchronize()
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = total_bytes / te.item() / 1e9
+        line["e2e"] = {"value": round(e2e, 3), "unit": "GB/s", "h2d_bytes_per_step": nbytes + len(blob),
+                       "d2h_bytes_per_step": len(blob) + nbytes}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(vals.cpu().numpy(), args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,148 @@
+"""compress / decompress and the CSZH container (reference archive.py).
+
+`compress(field, spec, mode)` and `decompress(blob)` are the drop-in
+entry points (archive.py:41, :121).  They run the whole pipeline on the GPU
+through hb_compress / hb_decompress.  `compress_device` / `decompress_device`
+are the device-resident variants (torch CUDA tensors in and out, no host
+copies) that the throughput benchmark measures.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+
+import numpy as np
+
+from . import _lib
+from .errors import ArchiveError
+from .field import ErrorBoundSpec, Field
+from .predictor import InterpConfig
+
+MAGIC = b"CSZH"
+VERSION = 1
+MODE_CR = "cr"
+MODE_TP = "tp"
+_MODE_BYTE = {MODE_CR: 0, MODE_TP: 1}
+_MODE_NAME = {0: MODE_CR, 1: MODE_TP}
+_FIXED = struct.Struct("<4sBBBBBB4sQQQd")
+_U64 = struct.Struct("<Q")
+
+
+def _prec(field: Field) -> int:
+    return field.dtype.itemsize
+
+
+def compress_bound(dims, precision: int) -> int:
+    n = C.c_size_t()
+    _lib.raise_for(_lib.lib().hb_compress_bound(_lib.dims3(dims), int(precision), C.byref(n)), None, "bad args")
+    return n.value
+
+
+def _compress_into(field: Field, spec: ErrorBoundSpec, mode: str, out, cap: int):
+    if mode not in _MODE_BYTE:
+        raise ValueError(f"mode must be {MODE_CR!r} or {MODE_TP!r}, got {mode!r}")
+    L, c = _lib.lib(), _lib.ctx()
+    olen = C.c_size_t()
+    eb = C.c_double()
+    cfg = (C.c_uint8 * 4)()
+    rc = L.hb_compress(c, _lib.ptr(field.values), _prec(field), _lib.dims3(field.dims), field.ndim,
+                       0 if spec.mode == "abs" else 1, float(spec.magnitude), _MODE_BYTE[mode], _lib.ptr(out), cap,
+                       C.byref(olen), C.byref(eb), cfg)
+    _lib.raise_for(rc, c)
+    return olen.value, eb.value, bytes(cfg)
+
+
+def compress(field: Field, spec: ErrorBoundSpec, mode: str = MODE_CR) -> bytes:
+    """Compress a field under the given error bound; returns archive bytes."""
+    if mode not in _MODE_BYTE:
+        raise ValueError(f"mode must be {MODE_CR!r} or {MODE_TP!r}, got {mode!r}")
+    cap = compress_bound(field.dims, _prec(field))
+    out = np.empty(cap, np.uint8)
+    n, _, _ = _compress_into(field, spec, mode, out, cap)
+    return out[:n].tobytes()
+
+
+def compress_device(field: Field, spec: ErrorBoundSpec, mode: str = MODE_CR, out=None):
+    """Device-resident compress: returns a uint8 CUDA tensor view of the archive."""
+    import torch
+    cap = compress_bound(field.dims, _prec(field))
+    if out is None or out.numel() < cap:
+        out = torch.empty(cap, dtype=torch.uint8, device=field.values.device)
+    n, _, _ = _compress_into(field, spec, mode, out, cap)
+    return out[:n]
+
+
+def _info(blob) -> "_lib.Info":
+    info = _lib.Info()
+    L = _lib.lib()
+    if _lib.is_cuda(blob):
+        return None
+    raw = bytes(blob) if not isinstance(blob, (bytes, np.ndarray)) else blob
+    arr = np.frombuffer(raw, np.uint8) if isinstance(raw, bytes) else raw
+    n = arr.size
+    keep = arr if n else np.zeros(1, np.uint8)
+    _lib.raise_for(L.hb_archive_info(_lib.ptr(keep), n, C.byref(info)), None, "archive")
+    return info
+
+
+def decompress(blob, out=None) -> Field:
+    """Decode an archive back into a field (host numpy values).
+
+    `out` optionally supplies the destination array (e.g. a pinned buffer)."""
+    data = bytes(blob)
+    arr = np.frombuffer(data, np.uint8) if data else np.zeros(1, np.uint8)
+    info = _lib.Info()
+    L = _lib.lib()
+    rc = L.hb_archive_info(_lib.ptr(arr), len(data), C.byref(info))
+    if rc:
+        # host-side header validation: same messages as the device path
+        c = _lib.ctx()
+        rc2 = L.hb_decompress(c, _lib.ptr(arr), len(data), _lib.ptr(arr), 0, None)
+        _lib.raise_for(rc2 if rc2 else rc, c)
+    dims = tuple(int(d) for d in info.dims)
+    dt = np.float32 if info.precision == 4 else np.float64
+    if out is None:
+        out = np.empty(dims, dt)
+    elif out.dtype != dt or tuple(out.shape) != dims or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a contiguous {np.dtype(dt)} array of shape {dims}")
+    c = _lib.ctx()
+    rc = L.hb_decompress(c, _lib.ptr(arr), len(data), _lib.ptr(out), out.nbytes, None)
+    _lib.raise_for(rc, c)
+    return Field(out, ndim=info.ndim)
+
+
+def decompress_device(archive, dims, dtype, ndim: int = 3, out=None):
+    """Device-resident decompress of a uint8 CUDA tensor archive into a CUDA tensor."""
+    import torch
+    tdt = torch.float32 if np.dtype(dtype) == np.float32 else torch.float64
+    if out is None:
+        out = torch.empty(tuple(dims), dtype=tdt, device=archive.device)
+    L, c = _lib.lib(), _lib.ctx()
+    rc = L.hb_decompress(c, _lib.ptr(archive), archive.numel(), _lib.ptr(out), out.numel() * out.element_size(), None)
+    _lib.raise_for(rc, c)
+    return Field(out, ndim=ndim)
+
+
+def section_sizes(blob: bytes) -> dict:
+    """Byte-level breakdown of an archive without decoding the stream (archive.py:174-200)."""
+    data = bytes(blob)
+    arr = np.frombuffer(data, np.uint8) if data else np.zeros(1, np.uint8)
+    info = _lib.Info()
+    rc = _lib.lib().hb_archive_info(_lib.ptr(arr), len(data), C.byref(info))
+    if rc:
+        raise ArchiveError("corrupt or truncated archive")
+    mode = _MODE_NAME[info.mode]
+    return {
+        "mode": mode, "precision": info.precision, "ndim": info.ndim,
+        "dims": tuple(int(d) for d in info.dims), "abs_eb": info.eb, "anchor_stride": info.stride,
+        "raw_escape": bool(info.escape), "header_bytes": _FIXED.size + 3 * 8,
+        "anchor_count": info.anchor_count, "anchor_bytes": info.anchor_count * info.precision,
+        "outlier_count": info.outlier_count, "outlier_bytes": info.outlier_count * (8 + info.precision),
+        "stream_bytes": info.stream_len, "total_bytes": len(data),
+        "huffman_table_bytes": 0 if (info.escape or mode != MODE_CR) else 256,
+    }
+
+
+def archive_config(blob: bytes) -> InterpConfig:
+    return InterpConfig.from_bytes(bytes(blob[10:14]))

@@ -1,0 +1,1184 @@
+// hb_api.cu -- the C ABI (include/hibound_b200.h): contexts, scratch arena,
+// and the device launch sequences of compress / decompress.
+//
+// One call = one asynchronous launch sequence on the context's stream with
+// every data-dependent size kept on the device; the host synchronises once at
+// the end to read the status block (flags, archive length) -- the only D2H
+// besides the result itself.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "hb_common.cuh"
+#include "hb_kernels.h"
+
+using namespace hb;
+
+
+
+struct hb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  uint8_t* arena = nullptr;
+  size_t arena_size = 0;
+  uint8_t* pinned = nullptr;
+  size_t pinned_size = 0;
+  std::string err;
+  uint64_t launches = 0;
+  // optional phase profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<const char*> ev_name;
+  int nev = 0;
+  std::vector<const char*> phase_name;
+  std::vector<float> phase_ms;
+  void mark(const char* name) {
+    if (!prof) return;
+    if (nev >= (int)ev.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+      ev_name.push_back(nullptr);
+    }
+    cudaEventRecord(ev[nev], stream);
+    ev_name[nev] = name;
+    nev++;
+  }
+  void collect() {
+    phase_name.clear();
+    phase_ms.clear();
+    if (!prof) return;
+    for (int i = 1; i < nev; i++) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      phase_name.push_back(ev_name[i]);
+      phase_ms.push_back(ms);
+    }
+    nev = 0;
+  }
+};
+
+namespace {
+
+int set_err(hb_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CU(call)                                                                                      \
+  do {                                                                                                \
+    cudaError_t e_ = (call);                                                                          \
+    if (e_ != cudaSuccess) return set_err(ctx, HB_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+int ilog2i(int a) {
+  int t = 0;
+  while ((1 << (t + 1)) <= a) t++;
+  return t;
+}
+
+int anchor_stride(const uint64_t d[3]) {  // predictor.py:114-124
+  uint64_t lim = 0;
+  for (int a = 0; a < 3; a++)
+    if (d[a] > 1 && (lim == 0 || d[a] < lim)) lim = d[a];
+  if (lim == 0) lim = 1;
+  const uint64_t cap = lim < 16 ? lim : 16;
+  int s = 1;
+  while ((uint64_t)(s * 2) <= cap) s *= 2;
+  return s;
+}
+
+// tuning.py:66-97
+int plan_blocks(const uint64_t dims[3], std::vector<unsigned long long>& org, int shape[3]) {
+  uint64_t mn = 0;
+  bool any = false;
+  for (int a = 0; a < 3; a++)
+    if (dims[a] > 1) {
+      if (!any || dims[a] < mn) mn = dims[a];
+      any = true;
+    }
+  org.clear();
+  if (!any || mn < 17) {
+    for (int a = 0; a < 3; a++) shape[a] = (int)dims[a];
+    org.push_back(0), org.push_back(0), org.push_back(0);
+    return 1;
+  }
+  uint64_t cnt[3];
+  for (int a = 0; a < 3; a++) {
+    shape[a] = dims[a] > 1 ? 17 : 1;
+    cnt[a] = dims[a] == 1 ? 1 : (dims[a] - shape[a]) / 16 + 1;
+  }
+  const uint64_t m = cnt[0] * cnt[1] * cnt[2];
+  const uint64_t total = dims[0] * dims[1] * dims[2];
+  const uint64_t bp = (uint64_t)shape[0] * shape[1] * shape[2];
+  uint64_t want = (total * 2 + bp * 1000 - 1) / (bp * 1000);
+  if (want < 1) want = 1;
+  if (want > m) want = m;
+  uint64_t prev = ~0ull;
+  int n = 0;
+  for (uint64_t i = 0; i < want; i++) {
+    const uint64_t ci = want == 1 ? m / 2 : (i * (m - 1)) / (want - 1);
+    if (ci == prev) continue;
+    prev = ci;
+    uint64_t o[3] = {(ci / (cnt[2] * cnt[1])) * 16, ((ci / cnt[2]) % cnt[1]) * 16, (ci % cnt[2]) * 16};
+    bool ok = true;
+    for (int p = 0; p < n && ok; p++) {
+      bool sep = false;
+      for (int a = 0; a < 3; a++) {
+        const uint64_t q = org[3 * p + a];
+        if ((o[a] > q ? o[a] - q : q - o[a]) >= (uint64_t)shape[a]) sep = true;
+      }
+      ok = sep;
+    }
+    if (!ok) continue;
+    for (int a = 0; a < 3; a++) org.push_back(o[a]);
+    n++;
+  }
+  return n;
+}
+
+enum MemKind { MEM_HOST = 0, MEM_DEVICE = 1 };
+MemKind mem_kind(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return MEM_HOST;
+  }
+  return (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) ? MEM_DEVICE : MEM_HOST;
+}
+
+// bump allocator over the context arena
+struct Layout {
+  size_t off = 0;
+  size_t take(size_t n) {
+    const size_t o = off;
+    off += (n + 255) & ~size_t(255);
+    return o;
+  }
+};
+
+int ensure_arena(hb_ctx* ctx, size_t need) {
+  if (ctx->arena_size >= need) return 0;
+  if (ctx->arena) cudaFree(ctx->arena);
+  ctx->arena = nullptr;
+  ctx->arena_size = 0;
+  const size_t sz = need + need / 8;
+  CU(cudaMalloc(&ctx->arena, sz));
+  ctx->arena_size = sz;
+  return 0;
+}
+
+int ensure_pinned(hb_ctx* ctx, size_t need) {
+  if (ctx->pinned_size >= need) return 0;
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  ctx->pinned = nullptr;
+  ctx->pinned_size = 0;
+  CU(cudaMallocHost(&ctx->pinned, need));
+  ctx->pinned_size = need;
+  return 0;
+}
+
+int flags_to_code(hb_ctx* ctx, uint32_t f, uint32_t detail) {
+  if (f & F_NONFINITE) return set_err(ctx, HB_EFIELD, "field contains NaN or Inf values");
+  if (f & F_DEGENERATE)
+    return set_err(ctx, HB_EBOUND,
+                   detail == 1 ? "relative error bound on a constant field (value range 0)"
+                               : "error bound must be positive and finite");
+  if (f & F_UNSUPPORTED) return set_err(ctx, HB_EUNSUPPORTED, "unsupported stream (detail %u)", detail);
+  if (f & F_CAPACITY) return set_err(ctx, HB_ECUDA, "internal capacity exceeded (detail %u)", detail);
+  if (f & F_STAGE) return set_err(ctx, HB_ESTAGE, "lossless stage record failed to decode (detail %u)", detail);
+  if (f & F_ORPHAN) return set_err(ctx, HB_EARCHIVE, "outlier marker without a matching outlier entry");
+  if (f & F_ZEROCOUNT) return set_err(ctx, HB_EARCHIVE, "outlier markers do not match the outlier section");
+  if (f & F_ARCHIVE) return set_err(ctx, HB_EARCHIVE, "corrupt archive (detail %u)", detail);
+  return HB_OK;
+}
+
+struct ChainBufs {
+  ReduceBufs rb;
+  uint8_t** table;  // device: 4 bitmaps, 4 payloads
+  unsigned long long max_words;
+};
+
+// sizes of one reducer chain over a source of at most max_bytes bytes / width
+void plan_chain(Layout& L, unsigned long long max_bytes, int width, size_t offs[9], unsigned long long* max_words) {
+  unsigned long long words = cdiv(max_bytes, width);
+  *max_words = words;
+  for (int k = 0; k < 4; k++) {
+    const int w = k == 0 ? width : 1;
+    offs[k] = L.take(cdiv(words, 32) * 4 + 512);  // bitmap
+    offs[4 + k] = L.take(words * w + 512);        // payload
+    words = cdiv(words, 8);
+  }
+  offs[8] = L.take(8 * sizeof(void*));
+}
+
+void bind_chain(uint8_t* base, const size_t offs[9], unsigned long long max_words, ChainBufs* cb,
+                std::vector<uint8_t*>& host_table) {
+  for (int k = 0; k < 4; k++) {
+    cb->rb.bitmap[k] = base + offs[k];
+    cb->rb.payload[k] = base + offs[4 + k];
+  }
+  cb->table = reinterpret_cast<uint8_t**>(base + offs[8]);
+  cb->max_words = max_words;
+  host_table.assign(8, nullptr);
+  for (int k = 0; k < 4; k++) host_table[k] = cb->rb.bitmap[k], host_table[4 + k] = cb->rb.payload[k];
+}
+
+unsigned long long lb_entries(unsigned long long items, unsigned long long tile) { return 2 + cdiv(items, tile); }
+
+struct HostStatus {
+  double eb;
+  uint32_t flags, detail;
+  uint8_t cfg[4];
+  double tune_errs[16];
+  unsigned long long outlier_count, zero_count, archive_len, stream_len;
+  int escape;
+};
+
+__global__ void k_status(const DevState* st, HostStatus* out) {
+  out->eb = st->eb;
+  out->flags = st->flags;
+  out->detail = st->detail;
+  for (int i = 0; i < 4; i++) out->cfg[i] = st->cfg[i];
+  for (int i = 0; i < 16; i++) out->tune_errs[i] = st->tune_errs[i];
+  out->outlier_count = st->outlier_count;
+  out->zero_count = st->zero_count;
+  out->archive_len = st->archive_len;
+  out->stream_len = st->stream_len;
+  out->escape = st->escape;
+}
+
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+__global__ void k_set_cfg_eb(DevState* st, uint8_t c0, uint8_t c1, uint8_t c2, uint8_t c3, double eb) {
+  st->cfg[0] = c0, st->cfg[1] = c1, st->cfg[2] = c2, st->cfg[3] = c3;
+  st->eb = eb;
+  st->two_eb = __dmul_rn(2.0, eb);
+}
+__global__ void k_check_len(const unsigned long long* len, unsigned long long want, DevState* st, uint32_t flag) {
+  if (!(st->flags & (F_STAGE | F_ARCHIVE)) && *len != want) raise_flag(st, flag, 200);
+}
+
+int read_status(hb_ctx* ctx, DevState* st, HostStatus* hs) {
+  HostStatus* dst = reinterpret_cast<HostStatus*>(ctx->pinned);
+  k_status<<<1, 1, 0, ctx->stream>>>(st, dst);
+  ctx->launches++;
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaGetLastError());
+  *hs = *dst;
+  return 0;
+}
+
+// archive.py:93-118 + section walk; `rd(off, n, dst)` fetches archive bytes
+template <class Reader>
+int parse_info_t(Reader rd, size_t len, hb_info* I, hb_ctx* ctx) {
+  memset(I, 0, sizeof *I);
+  uint8_t b[46];
+  auto u64at = [&](size_t off, uint64_t* v) -> int {
+    uint8_t t[8];
+    int r = rd(off, 8, t);
+    if (r) return r;
+    *v = 0;
+    for (int i = 0; i < 8; i++) *v |= (uint64_t)t[i] << (8 * i);
+    return 0;
+  };
+  auto u64 = [](const uint8_t* p) {
+    uint64_t v = 0;
+    for (int i = 0; i < 8; i++) v |= (uint64_t)p[i] << (8 * i);
+    return v;
+  };
+  int r;
+  if (len < 46) return set_err(ctx, HB_EARCHIVE, "archive truncated in header");
+  if ((r = rd(0, 46, b))) return r;
+  if (memcmp(b, "CSZH", 4)) return set_err(ctx, HB_EARCHIVE, "bad magic");
+  if (b[4] != 1) return set_err(ctx, HB_EARCHIVE, "unsupported archive version %d", b[4]);
+  if (b[5] > 1) return set_err(ctx, HB_EARCHIVE, "unknown mode byte %d", b[5]);
+  if (b[6] != 4 && b[6] != 8) return set_err(ctx, HB_EARCHIVE, "unsupported precision %d", b[6]);
+  if (b[7] != 2 && b[7] != 3) return set_err(ctx, HB_EARCHIVE, "unsupported ndim %d", b[7]);
+  const int st = b[8];
+  if (st < 1 || st > 16 || (st & (st - 1))) return set_err(ctx, HB_EARCHIVE, "invalid anchor stride %d", st);
+  if (b[9] > 1) return set_err(ctx, HB_EARCHIVE, "invalid escape flag %d", b[9]);
+  I->mode = b[5], I->precision = b[6], I->ndim = b[7], I->stride = st, I->escape = b[9];
+  memcpy(I->cfg, b + 10, 4);
+  for (int a = 0; a < 3; a++) I->dims[a] = u64(b + 14 + 8 * a);
+  uint64_t eb_bits = u64(b + 38);
+  memcpy(&I->eb, &eb_bits, 8);
+  for (int a = 0; a < 3; a++)
+    if (I->dims[a] < 1) return set_err(ctx, HB_EARCHIVE, "invalid dims");
+  if (I->ndim == 2 && I->dims[2] != 1) return set_err(ctx, HB_EARCHIVE, "2D archive must carry a trailing dimension of 1");
+  if (!(isfinite(I->eb) && I->eb > 0)) return set_err(ctx, HB_EARCHIVE, "invalid error bound");
+  for (int i = 0; i < 4; i++)
+    if (I->cfg[i] & ~3) return set_err(ctx, HB_EARCHIVE, "invalid interpolation config byte 0x%02x", I->cfg[i]);
+  size_t off = 46;
+  if (len - off < 8) return set_err(ctx, HB_EARCHIVE, "archive truncated in anchor count");
+  if ((r = u64at(off, &I->anchor_count))) return r;
+  off += 8;
+  unsigned __int128 ea = 1;
+  for (int a = 0; a < 3; a++) ea *= (I->dims[a] + st - 1) / st;
+  if ((unsigned __int128)I->anchor_count != ea)
+    return set_err(ctx, HB_EARCHIVE, "anchor count %llu does not match dims", (unsigned long long)I->anchor_count);
+  unsigned __int128 need = (unsigned __int128)I->anchor_count * I->precision;
+  if (need > len - off) return set_err(ctx, HB_EARCHIVE, "archive truncated in anchor values");
+  I->anchor_off = off;
+  off += (size_t)need;
+  if (len - off < 8) return set_err(ctx, HB_EARCHIVE, "archive truncated in outlier count");
+  if ((r = u64at(off, &I->outlier_count))) return r;
+  off += 8;
+  const unsigned __int128 n = (unsigned __int128)I->dims[0] * I->dims[1] * I->dims[2];
+  if ((unsigned __int128)I->outlier_count > n) return set_err(ctx, HB_EARCHIVE, "outlier count exceeds point count");
+  need = (unsigned __int128)I->outlier_count * (8 + I->precision);
+  if (need > len - off) return set_err(ctx, HB_EARCHIVE, "archive truncated in outlier section");
+  I->outlier_off = off;
+  off += (size_t)need;
+  if (len - off < 8) return set_err(ctx, HB_EARCHIVE, "archive truncated in stream length");
+  if ((r = u64at(off, &I->stream_len))) return r;
+  off += 8;
+  if (I->stream_len > len - off) return set_err(ctx, HB_EARCHIVE, "archive truncated in code stream");
+  I->stream_off = off;
+  off += (size_t)I->stream_len;
+  if (off != len) return set_err(ctx, HB_EARCHIVE, "%zu trailing bytes after code stream", len - off);
+  if (n > ((unsigned __int128)1 << 40)) return set_err(ctx, HB_EARCHIVE, "dims too large");
+  return HB_OK;
+}
+
+int parse_info(const uint8_t* blob, size_t len, hb_info* I, hb_ctx* ctx) {
+  return parse_info_t([&](size_t off, size_t n, uint8_t* dst) { memcpy(dst, blob + off, n); return 0; }, len, I,
+                      ctx);
+}
+
+struct Hdr46 {
+  uint8_t b[46];
+};
+
+int validate_field_args(hb_ctx* ctx, int precision, const uint64_t dims[3], int ndim) {
+  if (precision != 4 && precision != 8) return set_err(ctx, HB_EFIELD, "unsupported precision %d", precision);
+  if (ndim != 2 && ndim != 3) return set_err(ctx, HB_EFIELD, "ndim must be 2 or 3, got %d", ndim);
+  for (int a = 0; a < 3; a++)
+    if (dims[a] < 1) return set_err(ctx, HB_EFIELD, "empty dimension");
+  if (ndim == 2 && dims[2] != 1) return set_err(ctx, HB_EFIELD, "a 2D field must carry a trailing axis of size 1");
+  return HB_OK;
+}
+
+}  // namespace
+
+// =================================================================== ABI
+
+extern "C" {
+
+int hb_ctx_create(int device, void* cuda_stream, hb_ctx** out) {
+  hb_ctx* ctx = nullptr;
+  if (!out) return HB_EARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return HB_ECUDA;
+  }
+  if (device < 0 || device >= ndev) return HB_EARG;
+  ctx = new hb_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete ctx;
+    return HB_ECUDA;
+  }
+  if (cuda_stream) {
+    ctx->stream = (cudaStream_t)cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      return HB_ECUDA;
+    }
+    ctx->own_stream = true;
+  }
+  if (ensure_pinned(ctx, 1 << 16)) {
+    delete ctx;
+    return HB_ECUDA;
+  }
+  *out = ctx;
+  return HB_OK;
+}
+
+void hb_ctx_destroy(hb_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->arena) cudaFree(ctx->arena);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (auto e : ctx->ev) cudaEventDestroy(e);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* hb_last_error(const hb_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+void hb_profile(hb_ctx* ctx, int enable) {
+  if (ctx) ctx->prof = enable != 0;
+}
+
+int hb_last_phases(const hb_ctx* ctx, const char** names, float* ms, int cap) {
+  if (!ctx) return 0;
+  const int n = (int)ctx->phase_ms.size();
+  for (int i = 0; i < n && i < cap; i++) {
+    if (names) names[i] = ctx->phase_name[i];
+    if (ms) ms[i] = ctx->phase_ms[i];
+  }
+  return n;
+}
+uint64_t hb_last_launch_count(const hb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int hb_compress_bound(const uint64_t dims[3], int precision, size_t* max_bytes) {
+  if (!dims || !max_bytes || (precision != 4 && precision != 8)) return HB_EARG;
+  const uint64_t n = dims[0] * dims[1] * dims[2];
+  const int A = anchor_stride(dims);
+  uint64_t na = 1;
+  for (int a = 0; a < 3; a++) na *= (dims[a] + A - 1) / A;
+  *max_bytes = 46 + 8 + na * precision + 8 + n * (8 + precision) + 8 + n;
+  return HB_OK;
+}
+
+int hb_archive_info(const void* host_blob, size_t len, hb_info* info) {
+  if (!host_blob || !info) return HB_EARG;
+  return parse_info((const uint8_t*)host_blob, len, info, nullptr);
+}
+
+// ------------------------------------------------------------- compress
+
+static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_t dims[3], int ndim, int eb_mode,
+                         double mag, int mode, void* out, size_t cap, size_t* out_len, double* abs_eb_out,
+                         uint8_t cfg_out[4], double* tune_errs_out, bool tune_only) {
+  int rc = validate_field_args(ctx, prec, dims, ndim);
+  if (rc) return rc;
+  if (mode != 0 && mode != 1) return set_err(ctx, HB_EARG, "mode must be 'cr' or 'tp'");
+  if (eb_mode != 0 && eb_mode != 1) return set_err(ctx, HB_EBOUND, "error-bound mode must be 'abs' or 'rel'");
+  if (!(isfinite(mag) && mag > 0)) return set_err(ctx, HB_EBOUND, "error-bound magnitude must be positive, got %g", mag);
+  cudaSetDevice(ctx->device);
+  const cudaStream_t s = ctx->stream;
+  const unsigned long long N = dims[0] * dims[1] * dims[2];
+  const int A = anchor_stride(dims), top = ilog2i(A);
+  unsigned long long na = 1;
+  for (int a = 0; a < 3; a++) na *= (dims[a] + A - 1) / A;
+  // tuner plan (host, deterministic)
+  std::vector<unsigned long long> org;
+  TunePlan tp;
+  tp.nb = plan_blocks(dims, org, tp.shape);
+  tp.bn = (unsigned long long)tp.shape[0] * tp.shape[1] * tp.shape[2];
+  tp.top = ilog2i(anchor_stride(std::vector<uint64_t>{(uint64_t)tp.shape[0], (uint64_t)tp.shape[1],
+                                                      (uint64_t)tp.shape[2]}.data()));
+  if (tp.top > 0 && !tune_supported(tp))
+    return set_err(ctx, HB_EUNSUPPORTED, "thin field: whole-field tuner block of %llu points is too large",
+                   (unsigned long long)tp.bn);
+  size_t bound;
+  hb_compress_bound(dims, prec, &bound);
+  // ---- layout
+  Layout L;
+  const size_t o_st = L.take(sizeof(DevState));
+  const size_t o_field = mem_kind(field) == MEM_HOST ? L.take(N * prec + 64) : 0;
+  const bool stage_field = mem_kind(field) == MEM_HOST;
+  unsigned long long ne = 1;
+  for (int a = 0; a < 3; a++) ne *= (dims[a] + 1) / 2;
+  const size_t o_E = L.take(ne * 8 + 64);
+  const size_t o_seq = L.take(N + 128);
+  const size_t o_obm = L.take(cdiv(N, 32) * 4 + 64);
+  const size_t o_org = L.take(org.size() * 8 + 8);
+  const size_t o_trials = L.take((size_t)2 * 4 * tp.nb * tp.bn * 8);
+  const size_t o_berr = L.take((size_t)4 * tp.nb * 8);
+  const size_t o_arch = L.take(bound + N / 4 + 4096);
+  const unsigned long long hf_max = 274 + N + 64;
+  const size_t o_hf = L.take(hf_max + 64);
+  size_t c1[9], c2[9];
+  unsigned long long w1, w2;
+  // CR: RRE4 over HF record; RZE1 over TCMS8(RRE4 record). TP: RRE1 over BIT1(TCMS1(seq)).
+  const unsigned long long rre4_max = hf_max + cdiv(hf_max, 32) + 4 * 64 + 64;
+  if (mode == 0) {
+    plan_chain(L, hf_max, 4, c1, &w1);
+    plan_chain(L, 10 + cdiv(rre4_max, 8) * 8 + 8, 1, c2, &w2);
+  } else {
+    plan_chain(L, 10 + cdiv(N + 10, 8) * 8, 1, c1, &w1);
+    w2 = 0;
+  }
+  const size_t o_rre4 = L.take(rre4_max + 64);
+  // look-back workspaces
+  const unsigned long long lb_oc = lb_entries(cdiv(N, 32), 8192);
+  const unsigned long long lb_he = lb_entries(N, 8192);
+  const unsigned long long lb_c1 = lb_entries(w1, 8192), lb_c2 = lb_entries(w2 ? w2 : 1, 8192);
+  const size_t o_lb = L.take((lb_oc + lb_he + 4 * lb_c1 + 4 * lb_c2) * 8);
+  const size_t lb_bytes = (lb_oc + lb_he + 4 * lb_c1 + 4 * lb_c2) * 8;
+  rc = ensure_arena(ctx, L.off);
+  if (rc) return rc;
+  rc = ensure_pinned(ctx, 1 << 16);
+  if (rc) return rc;
+  uint8_t* base = ctx->arena;
+  DevState* st = reinterpret_cast<DevState*>(base + o_st);
+  double* E = reinterpret_cast<double*>(base + o_E);
+  uint8_t* seq = base + o_seq;
+  uint32_t* obm = reinterpret_cast<uint32_t*>(base + o_obm);
+  unsigned long long* d_org = reinterpret_cast<unsigned long long*>(base + o_org);
+  double* trials = reinterpret_cast<double*>(base + o_trials);
+  double* berr = reinterpret_cast<double*>(base + o_berr);
+  uint8_t* arch = base + o_arch;
+  uint8_t* hf = base + o_hf;
+  uint8_t* rre4 = base + o_rre4;
+  unsigned long long* lb = reinterpret_cast<unsigned long long*>(base + o_lb);
+  ChainBufs cb1, cb2;
+  std::vector<uint8_t*> t1, t2;
+  bind_chain(base, c1, w1, &cb1, t1);
+  if (mode == 0) bind_chain(base, c2, w2, &cb2, t2);
+  int nl = 0;
+  const void* dfield = field;
+  if (stage_field) {
+    CU(cudaMemcpyAsync(base + o_field, field, N * prec, cudaMemcpyHostToDevice, s));
+    dfield = base + o_field;
+  }
+  CU(cudaMemsetAsync(st, 0, sizeof(DevState), s));
+  CU(cudaMemsetAsync(obm, 0, cdiv(N, 32) * 4 + 64, s));
+  CU(cudaMemsetAsync(lb, 0, lb_bytes, s));
+  CU(cudaMemcpyAsync(d_org, org.data(), org.size() * 8, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(cb1.table, t1.data(), 8 * sizeof(void*), cudaMemcpyHostToDevice, s));
+  if (mode == 0) CU(cudaMemcpyAsync(cb2.table, t2.data(), 8 * sizeof(void*), cudaMemcpyHostToDevice, s));
+  ctx->nev = 0;
+  ctx->mark("start");
+  // 1) error bound (field.py:135-142)
+  launch_minmax(dfield, prec, N, st, eb_mode, mag, s, &nl);
+  ctx->mark("eb_range");
+  // 2) tuner (tuning.py:105-150)
+  for (int level = tp.top; level >= 1; level--) {
+    launch_tune_level(tp, dfield, prec, dims, d_org, level, trials, berr, st, s, &nl);
+    launch_tune_select(tp, level, berr, st, s, &nl);
+  }
+  ctx->mark("tune");
+  if (!tune_only) {
+    // 3) anchors + the level walk with fused quantize / reorder / histogram
+    const unsigned long long abase = 46 + 8;
+    launch_anchor_init(dfield, prec, dims, A, E, seq, arch + abase, st, true, s, &nl);
+    static const char* lvl_names[5] = {"", "level1", "level2", "level3", "level4"};
+    for (int level = top; level >= 1; level--) {
+      LevelGeom g;
+      make_level_geom(dims, level, &g);
+      launch_level_compress(g, dfield, prec, E, seq, obm, st, s, &nl);
+      ctx->mark(lvl_names[level]);
+    }
+    // 4) outliers straight into the archive (archive.py:65-71)
+    const unsigned long long obase = abase + na * prec + 8;
+    launch_outlier_compact(obm, N, dfield, prec, arch + obase, nullptr, nullptr, lb, st, s, &nl);
+    launch_stream_offset(obase, prec, st, s, &nl);
+    k_set_u64<<<1, 1, 0, s>>>(&st->seq_len, N);
+    nl++;
+    ctx->mark("outliers");
+    unsigned long long* lbx = lb + lb_oc;
+    // 5) lossless pipeline, final record assembled in place at the stream offset
+    if (mode == 0) {
+      launch_huffman_build(st, N, hf, s, &nl);
+      ctx->mark("huff_build");
+      launch_huffman_encode(seq, N, hf, lbx, st, s, &nl);
+      ctx->mark("huff_encode");
+      lbx += lb_he;
+      launch_reduce_chain_impl(2, 4, SRC_MEM, hf, &st->hf_rec_len, 0, cb1.max_words, cb1.rb, &st->bm[0], rre4,
+                               nullptr, &st->scratch[1], lbx, lb_c1, cb1.table, s, &nl);
+      lbx += 4 * lb_c1;
+      launch_reduce_chain_impl(3, 1, SRC_TCMS, rre4, &st->scratch[1], 8, cb2.max_words, cb2.rb, &st->bm[1], arch,
+                               &st->scratch[0], &st->stream_len, lbx, lb_c2, cb2.table, s, &nl);
+    } else {
+      lbx += lb_he;
+      launch_reduce_chain_impl(2, 1, SRC_TP, seq, &st->seq_len, 0, cb1.max_words, cb1.rb, &st->bm[2], arch,
+                               &st->scratch[0], &st->stream_len, lbx, lb_c1, cb1.table, s, &nl);
+    }
+    // 6) escape decision, header, counts (archive.py:55-74)
+    Hdr46 h;
+    memset(&h, 0, sizeof h);
+    memcpy(h.b, "CSZH", 4);
+    h.b[4] = 1;
+    h.b[5] = (uint8_t)mode;
+    h.b[6] = (uint8_t)prec;
+    h.b[7] = (uint8_t)ndim;
+    h.b[8] = (uint8_t)A;
+    for (int a = 0; a < 3; a++)
+      for (int i = 0; i < 8; i++) h.b[14 + 8 * a + i] = (uint8_t)(dims[a] >> (8 * i));
+    uint8_t* d_h = reinterpret_cast<uint8_t*>(&st->scratch[8]);  // 46 bytes inside DevState scratch
+    CU(cudaMemcpyAsync(d_h, h.b, 46, cudaMemcpyHostToDevice, s));
+    ctx->mark("lossless");
+    launch_archive_tail_impl(arch, obase, prec, seq, N, d_h, na, st, s, &nl);
+    ctx->mark("archive");
+  }
+  ctx->launches = nl;
+  HostStatus hs;
+  rc = read_status(ctx, st, &hs);
+  ctx->collect();
+  if (rc) return rc;
+  rc = flags_to_code(ctx, hs.flags, hs.detail);
+  if (rc) return rc;
+  if (abs_eb_out) *abs_eb_out = hs.eb;
+  if (cfg_out) memcpy(cfg_out, hs.cfg, 4);
+  if (tune_errs_out) memcpy(tune_errs_out, hs.tune_errs, sizeof hs.tune_errs);
+  if (tune_only) return HB_OK;
+  if (hs.archive_len > cap) {
+    if (out_len) *out_len = hs.archive_len;
+    return set_err(ctx, HB_EARG, "output capacity %zu < archive length %llu", cap, hs.archive_len);
+  }
+  CU(cudaMemcpyAsync(out, arch, hs.archive_len, cudaMemcpyDefault, s));
+  CU(cudaStreamSynchronize(s));
+  if (out_len) *out_len = hs.archive_len;
+  return HB_OK;
+}
+
+int hb_compress(hb_ctx* ctx, const void* field, int precision, const uint64_t dims[3], int ndim, int eb_mode,
+                double eb, int mode, void* out, size_t cap, size_t* out_len, double* abs_eb_out,
+                uint8_t cfg_out[4]) {
+  if (!ctx || !field || !dims || !out) return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
+  return compress_impl(ctx, field, precision, dims, ndim, eb_mode, eb, mode, out, cap, out_len, abs_eb_out, cfg_out,
+                       nullptr, false);
+}
+
+int hb_tune(hb_ctx* ctx, const void* field, int precision, const uint64_t dims[3], double eb, uint8_t cfg_out[4],
+            double errs_out[16]) {
+  if (!ctx || !field || !dims) return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
+  for (int i = 0; i < 16; i++) errs_out[i] = NAN;
+  double tmp[16];
+  uint8_t dummy;
+  int rc = compress_impl(ctx, field, precision, dims, 3, 0, eb, 0, &dummy, 0, nullptr, nullptr, cfg_out, tmp, true);
+  if (rc) return rc;
+  // untuned levels stay NaN (tuning.py only reports levels top..1 of the block)
+  std::vector<unsigned long long> org;
+  int shp[3];
+  plan_blocks(dims, org, shp);
+  const uint64_t sd[3] = {(uint64_t)shp[0], (uint64_t)shp[1], (uint64_t)shp[2]};
+  const int top = ilog2i(anchor_stride(sd));
+  for (int l = 1; l <= top; l++)
+    for (int i = 0; i < 4; i++) errs_out[(l - 1) * 4 + i] = tmp[(l - 1) * 4 + i];
+  return HB_OK;
+}
+
+// ----------------------------------------------------------- decompress
+
+int hb_decompress(hb_ctx* ctx, const void* archive, size_t len, void* field_out, size_t cap, hb_info* info_out) {
+  if (!ctx || !archive || !field_out) return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
+  cudaSetDevice(ctx->device);
+  const cudaStream_t s = ctx->stream;
+  const bool host_arch = mem_kind(archive) == MEM_HOST;
+  hb_info I;
+  int rc;
+  if (host_arch) {
+    rc = parse_info((const uint8_t*)archive, len, &I, ctx);
+  } else {
+    // header fields live in device memory: fetch the few bytes the walk needs
+    rc = parse_info_t(
+        [&](size_t off, size_t n, uint8_t* dst) -> int {
+          cudaError_t e = cudaMemcpy(dst, (const uint8_t*)archive + off, n, cudaMemcpyDeviceToHost);
+          return e == cudaSuccess ? 0 : set_err(ctx, HB_ECUDA, "cudaMemcpy: %s", cudaGetErrorString(e));
+        },
+        len, &I, ctx);
+  }
+  if (rc) return rc;
+  if (info_out) *info_out = I;
+  const unsigned long long N = I.dims[0] * I.dims[1] * I.dims[2];
+  const int prec = I.precision;
+  if (cap < N * prec) return set_err(ctx, HB_EARG, "output capacity %zu < %llu", cap, N * prec);
+  const int A = I.stride, top = ilog2i(A);
+  // ---- layout
+  Layout L;
+  const size_t o_st = L.take(sizeof(DevState));
+  const size_t o_arch = host_arch ? L.take(len + 64) : 0;
+  const size_t o_out = mem_kind(field_out) == MEM_HOST ? L.take(N * prec + 64) : 0;
+  unsigned long long ne = 1;
+  for (int a = 0; a < 3; a++) ne *= (I.dims[a] + 1) / 2;
+  const size_t o_E = L.take(ne * 8 + 64);
+  const size_t o_seq = L.take(N + 128);
+  const size_t o_oidx = L.take(I.outlier_count * 8 + 64);
+  const size_t o_oval = L.take(I.outlier_count * 8 + 64);
+  const unsigned long long cap_rec = N + N / 8 + 4096;  // bound on valid intermediate records
+  size_t o_tmp[4], o_a = 0, o_b = 0, o_c = 0, o_bmd = 0, o_hd = 0;
+  unsigned long long wb = cap_rec;
+  for (int k = 0; k < 4; k++) {
+    o_tmp[k] = L.take(wb + 512);
+    wb = cdiv(wb, 8) + 64;
+  }
+  o_a = L.take(cap_rec + 512);
+  o_b = L.take(cap_rec + 512);
+  o_c = L.take(cap_rec + 512);
+  o_bmd = L.take(1024);
+  const size_t hd_bytes = huffman_decode_ws_bytes(cap_rec);
+  o_hd = L.take(hd_bytes);
+  const unsigned long long lbn = lb_entries(cap_rec, 8192);
+  const size_t o_lb = L.take(lbn * 8 * 12);
+  rc = ensure_arena(ctx, L.off);
+  if (rc) return rc;
+  uint8_t* base = ctx->arena;
+  DevState* st = reinterpret_cast<DevState*>(base + o_st);
+  const uint8_t* arch = host_arch ? base + o_arch : (const uint8_t*)archive;
+  void* out = o_out ? (void*)(base + o_out) : field_out;
+  double* E = reinterpret_cast<double*>(base + o_E);
+  uint8_t* seq = base + o_seq;
+  uint64_t* oidx = reinterpret_cast<uint64_t*>(base + o_oidx);
+  double* oval = reinterpret_cast<double*>(base + o_oval);
+  uint8_t* tmp[4];
+  for (int k = 0; k < 4; k++) tmp[k] = base + o_tmp[k];
+  uint8_t *ta = base + o_a, *tb = base + o_b, *tc = base + o_c;
+  unsigned long long* lb = reinterpret_cast<unsigned long long*>(base + o_lb);
+  int nl = 0;
+  if (host_arch) CU(cudaMemcpyAsync(base + o_arch, archive, len, cudaMemcpyHostToDevice, s));
+  CU(cudaMemsetAsync(st, 0, sizeof(DevState), s));
+  CU(cudaMemsetAsync(lb, 0, lbn * 8 * 12, s));
+  CU(cudaMemsetAsync(base + o_hd, 0, hd_bytes, s));
+  ctx->nev = 0;
+  ctx->mark("start");
+  k_set_cfg_eb<<<1, 1, 0, s>>>(st, I.cfg[0], I.cfg[1], I.cfg[2], I.cfg[3], I.eb);
+  nl++;
+  k_set_u64<<<1, 1, 0, s>>>(&st->scratch[2], I.stream_len);
+  nl++;
+  k_set_u64<<<1, 1, 0, s>>>(&st->scratch[3], I.outlier_count);
+  nl++;
+  // outliers (archive.py:136-150)
+  if (I.outlier_count) {
+    launch_outliers_parse(arch + I.outlier_off, prec, I.outlier_count, &st->scratch[3], N, oidx, oval, st, s, &nl);
+  }
+  // code stream -> level-grouped sequence (archive.py:157-164)
+  const uint8_t* stream = arch + I.stream_off;
+  const uint8_t* codes = seq;
+  unsigned long long* lbx = lb;
+  if (I.escape) {
+    if (I.stream_len != N) return set_err(ctx, HB_EARCHIVE, "decoded code sequence has %llu bytes, expected %llu",
+                                          (unsigned long long)I.stream_len, N);
+    codes = stream;
+    launch_count_zeros(stream, N, st, s, &nl);
+  } else if (I.mode == 0) {
+    // CR: huffman <- rre <- tcms <- rze (stages.py:426-427)
+    launch_reduce_decode_impl(3, stream, &st->scratch[2], cap_rec, ta, &st->scratch[4], tmp, base + o_bmd, lbx, lbn,
+                              st, s, &nl);
+    lbx += 4 * lbn;
+    launch_tcms_decode(ta, &st->scratch[4], cap_rec, tb, &st->scratch[5], st, s, &nl);
+    launch_reduce_decode_impl(2, tb, &st->scratch[5], cap_rec, tc, &st->scratch[6], tmp, base + o_bmd, lbx, lbn, st,
+                              s, &nl);
+    lbx += 4 * lbn;
+    ctx->mark("decode_bitmaps");
+    launch_huffman_decode_impl(tc, &st->scratch[6], N, N, cap_rec, seq, base + o_hd, lbx, st, s, &nl);
+  } else {
+    // TP: tcms <- bit <- rre (stages.py:434-435)
+    launch_reduce_decode_impl(2, stream, &st->scratch[2], cap_rec, ta, &st->scratch[4], tmp, base + o_bmd, lbx, lbn,
+                              st, s, &nl);
+    lbx += 4 * lbn;
+    launch_bit_decode(ta, &st->scratch[4], tb, &st->scratch[5], cap_rec, st, s, &nl);
+    launch_tcms_decode(tb, &st->scratch[5], cap_rec, seq, &st->scratch[6], st, s, &nl);
+    k_check_len<<<1, 1, 0, s>>>(&st->scratch[6], N, st, F_ARCHIVE);
+    nl++;
+    launch_count_zeros(seq, N, st, s, &nl);
+  }
+  ctx->mark("decode_stream");
+  // reconstruct (predictor.py:378-416) with fused inverse reorder
+  if (top == 0) {
+    launch_copy_anchors_out(arch + I.anchor_off, prec, N, out, s, &nl);
+  } else {
+    launch_anchor_load(arch + I.anchor_off, prec, I.dims, A, E, s, &nl);
+    for (int level = top; level >= 1; level--) {
+      LevelGeom g;
+      make_level_geom(I.dims, level, &g);
+      launch_level_decompress(g, codes, oidx, oval, &st->scratch[3], E, out, prec, st, s, &nl);
+      static const char* dl_names[5] = {"", "rlevel1", "rlevel2", "rlevel3", "rlevel4"};
+      ctx->mark(dl_names[level]);
+    }
+  }
+  ctx->launches = nl;
+  HostStatus hs;
+  rc = read_status(ctx, st, &hs);
+  ctx->collect();
+  if (rc) return rc;
+  // stage failures first (they happen before the marker check in the reference)
+  if (hs.flags & (F_STAGE | F_UNSUPPORTED | F_CAPACITY)) return flags_to_code(ctx, hs.flags, hs.detail);
+  if (hs.flags & F_ARCHIVE) return flags_to_code(ctx, hs.flags, hs.detail);
+  if (hs.zero_count != I.outlier_count)
+    return set_err(ctx, HB_EARCHIVE, "outlier markers do not match the outlier section");
+  rc = flags_to_code(ctx, hs.flags, hs.detail);
+  if (rc) return rc;
+  if (o_out) {
+    CU(cudaMemcpyAsync(field_out, out, N * prec, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+  }
+  return HB_OK;
+}
+
+// ------------------------------------------------------ parity hooks
+
+int hb_decompose(hb_ctx* ctx, const void* field, int prec, const uint64_t dims[3], double eb, const uint8_t cfg[4],
+                 uint8_t* seq_out, uint64_t* oidx_out, void* oval_out, uint64_t* ocount, void* anchors_out) {
+  if (!ctx || !field || !dims || !cfg || !seq_out) return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
+  int rc = validate_field_args(ctx, prec, dims, dims[2] == 1 ? 2 : 3);
+  if (rc) return rc;
+  if (!(isfinite(eb) && eb > 0)) return set_err(ctx, HB_EBOUND, "error bound must be positive and finite, got %g", eb);
+  cudaSetDevice(ctx->device);
+  const cudaStream_t s = ctx->stream;
+  const unsigned long long N = dims[0] * dims[1] * dims[2];
+  const int A = anchor_stride(dims), top = ilog2i(A);
+  unsigned long long na = 1, ne = 1;
+  for (int a = 0; a < 3; a++) na *= (dims[a] + A - 1) / A, ne *= (dims[a] + 1) / 2;
+  Layout L;
+  const size_t o_st = L.take(sizeof(DevState));
+  const size_t o_field = L.take(N * prec + 64);
+  const size_t o_E = L.take(ne * 8 + 64);
+  const size_t o_seq = L.take(N + 128);
+  const size_t o_obm = L.take(cdiv(N, 32) * 4 + 64);
+  const size_t o_oidx = L.take(N * 8 + 64);
+  const size_t o_oval = L.take(N * prec + 64);
+  const size_t o_anc = L.take(na * prec + 64);
+  const unsigned long long lbn = lb_entries(cdiv(N, 32), 8192);
+  const size_t o_lb = L.take(lbn * 8);
+  rc = ensure_arena(ctx, L.off);
+  if (rc) return rc;
+  uint8_t* base = ctx->arena;
+  DevState* st = reinterpret_cast<DevState*>(base + o_st);
+  const void* dfield = field;
+  if (mem_kind(field) == MEM_HOST) {
+    CU(cudaMemcpyAsync(base + o_field, field, N * prec, cudaMemcpyHostToDevice, s));
+    dfield = base + o_field;
+  }
+  int nl = 0;
+  CU(cudaMemsetAsync(st, 0, sizeof(DevState), s));
+  CU(cudaMemsetAsync(base + o_obm, 0, cdiv(N, 32) * 4 + 64, s));
+  CU(cudaMemsetAsync(base + o_lb, 0, lbn * 8, s));
+  k_set_cfg_eb<<<1, 1, 0, s>>>(st, cfg[0], cfg[1], cfg[2], cfg[3], eb);
+  nl++;
+  double* E = reinterpret_cast<double*>(base + o_E);
+  uint8_t* seq = base + o_seq;
+  launch_anchor_init(dfield, prec, dims, A, E, seq, base + o_anc, st, false, s, &nl);
+  for (int level = top; level >= 1; level--) {
+    LevelGeom g;
+    make_level_geom(dims, level, &g);
+    launch_level_compress(g, dfield, prec, E, seq, reinterpret_cast<uint32_t*>(base + o_obm), st, s, &nl);
+  }
+  launch_outlier_compact(reinterpret_cast<uint32_t*>(base + o_obm), N, dfield, prec, nullptr,
+                         reinterpret_cast<uint64_t*>(base + o_oidx), base + o_oval,
+                         reinterpret_cast<unsigned long long*>(base + o_lb), st, s, &nl);
+  ctx->launches = nl;
+  HostStatus hs;
+  rc = read_status(ctx, st, &hs);
+  if (rc) return rc;
+  if ((rc = flags_to_code(ctx, hs.flags, hs.detail))) return rc;
+  CU(cudaMemcpyAsync(seq_out, seq, N, cudaMemcpyDefault, s));
+  if (oidx_out) CU(cudaMemcpyAsync(oidx_out, base + o_oidx, hs.outlier_count * 8, cudaMemcpyDefault, s));
+  if (oval_out) CU(cudaMemcpyAsync(oval_out, base + o_oval, hs.outlier_count * prec, cudaMemcpyDefault, s));
+  if (anchors_out) CU(cudaMemcpyAsync(anchors_out, base + o_anc, na * prec, cudaMemcpyDefault, s));
+  CU(cudaStreamSynchronize(s));
+  if (ocount) *ocount = hs.outlier_count;
+  return HB_OK;
+}
+
+int hb_reconstruct(hb_ctx* ctx, const uint8_t* seq_in, const uint64_t* oidx_in, const void* oval_in,
+                   uint64_t ocount, const void* anchors, int prec, const uint64_t dims[3], int stride, double eb,
+                   const uint8_t cfg[4], void* field_out) {
+  if (!ctx || !seq_in || !anchors || !dims || !cfg || !field_out)
+    return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
+  if (!(isfinite(eb) && eb > 0)) return set_err(ctx, HB_EBOUND, "error bound must be positive and finite, got %g", eb);
+  if (stride < 1 || stride > 16 || (stride & (stride - 1))) return set_err(ctx, HB_EARG, "bad stride");
+  cudaSetDevice(ctx->device);
+  const cudaStream_t s = ctx->stream;
+  const unsigned long long N = dims[0] * dims[1] * dims[2];
+  const int A = stride, top = ilog2i(A);
+  unsigned long long na = 1, ne = 1;
+  for (int a = 0; a < 3; a++) na *= (dims[a] + A - 1) / A, ne *= (dims[a] + 1) / 2;
+  Layout L;
+  const size_t o_st = L.take(sizeof(DevState));
+  const size_t o_E = L.take(ne * 8 + 64);
+  const size_t o_seq = L.take(N + 128);
+  const size_t o_oidx = L.take(ocount * 8 + 64);
+  const size_t o_ovin = L.take(ocount * prec + 64);
+  const size_t o_oval = L.take(ocount * 8 + 64);
+  const size_t o_anc = L.take(na * prec + 64);
+  const size_t o_out = L.take(N * prec + 64);
+  int rc = ensure_arena(ctx, L.off);
+  if (rc) return rc;
+  uint8_t* base = ctx->arena;
+  DevState* st = reinterpret_cast<DevState*>(base + o_st);
+  int nl = 0;
+  CU(cudaMemsetAsync(st, 0, sizeof(DevState), s));
+  CU(cudaMemcpyAsync(base + o_seq, seq_in, N, cudaMemcpyDefault, s));
+  if (ocount) {
+    CU(cudaMemcpyAsync(base + o_oidx, oidx_in, ocount * 8, cudaMemcpyDefault, s));
+    CU(cudaMemcpyAsync(base + o_ovin, oval_in, ocount * prec, cudaMemcpyDefault, s));
+  }
+  CU(cudaMemcpyAsync(base + o_anc, anchors, na * prec, cudaMemcpyDefault, s));
+  k_set_cfg_eb<<<1, 1, 0, s>>>(st, cfg[0], cfg[1], cfg[2], cfg[3], eb);
+  nl++;
+  k_set_u64<<<1, 1, 0, s>>>(&st->scratch[3], ocount);
+  nl++;
+  // outlier values to f64 through the archive record parser layout: pack pairs
+  if (ocount) {
+    std::vector<uint8_t> rec(ocount * (8 + prec));
+    std::vector<uint8_t> hidx(ocount * 8), hval(ocount * prec);
+    CU(cudaMemcpyAsync(hidx.data(), base + o_oidx, ocount * 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(hval.data(), base + o_ovin, ocount * prec, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    for (uint64_t i = 0; i < ocount; i++) {
+      memcpy(&rec[i * (8 + prec)], &hidx[i * 8], 8);
+      memcpy(&rec[i * (8 + prec) + 8], &hval[i * prec], prec);
+    }
+    uint8_t* drec = base + o_out;  // temporarily reuse the output region
+    CU(cudaMemcpyAsync(drec, rec.data(), rec.size(), cudaMemcpyHostToDevice, s));
+    launch_outliers_parse(drec, prec, ocount, &st->scratch[3], N, reinterpret_cast<uint64_t*>(base + o_oidx),
+                          reinterpret_cast<double*>(base + o_oval), st, s, &nl);
+    CU(cudaStreamSynchronize(s));
+  }
+  void* out = mem_kind(field_out) == MEM_HOST ? (void*)(base + o_out) : field_out;
+  if (top == 0) {
+    launch_copy_anchors_out(base + o_anc, prec, N, out, s, &nl);
+  } else {
+    launch_anchor_load(base + o_anc, prec, dims, A, reinterpret_cast<double*>(base + o_E), s, &nl);
+    for (int level = top; level >= 1; level--) {
+      LevelGeom g;
+      make_level_geom(dims, level, &g);
+      launch_level_decompress(g, base + o_seq, reinterpret_cast<uint64_t*>(base + o_oidx),
+                              reinterpret_cast<double*>(base + o_oval), &st->scratch[3],
+                              reinterpret_cast<double*>(base + o_E), out, prec, st, s, &nl);
+    }
+  }
+  ctx->launches = nl;
+  HostStatus hs;
+  rc = read_status(ctx, st, &hs);
+  if (rc) return rc;
+  if ((rc = flags_to_code(ctx, hs.flags, hs.detail))) return rc;
+  if (out != field_out) {
+    CU(cudaMemcpyAsync(field_out, out, N * prec, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+  }
+  return HB_OK;
+}
+
+int hb_reorder(hb_ctx* ctx, const uint8_t* codes, const uint64_t dims[3], int stride, uint8_t* seq_out) {
+  if (!ctx || !codes || !dims || !seq_out) return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
+  cudaSetDevice(ctx->device);
+  const unsigned long long N = dims[0] * dims[1] * dims[2];
+  Layout L;
+  const size_t o_in = L.take(N + 64), o_out = L.take(N + 64);
+  int rc = ensure_arena(ctx, L.off);
+  if (rc) return rc;
+  int nl = 0;
+  CU(cudaMemcpyAsync(ctx->arena + o_in, codes, N, cudaMemcpyDefault, ctx->stream));
+  launch_reorder(ctx->arena + o_in, dims, stride, ctx->arena + o_out, false, ctx->stream, &nl);
+  CU(cudaMemcpyAsync(seq_out, ctx->arena + o_out, N, cudaMemcpyDefault, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->launches = nl;
+  return HB_OK;
+}
+
+int hb_inverse_reorder(hb_ctx* ctx, const uint8_t* seq, const uint64_t dims[3], int stride, uint8_t* codes_out) {
+  if (!ctx || !seq || !dims || !codes_out) return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
+  cudaSetDevice(ctx->device);
+  const unsigned long long N = dims[0] * dims[1] * dims[2];
+  Layout L;
+  const size_t o_in = L.take(N + 64), o_out = L.take(N + 64);
+  int rc = ensure_arena(ctx, L.off);
+  if (rc) return rc;
+  int nl = 0;
+  CU(cudaMemcpyAsync(ctx->arena + o_in, seq, N, cudaMemcpyDefault, ctx->stream));
+  launch_reorder(ctx->arena + o_in, dims, stride, ctx->arena + o_out, true, ctx->stream, &nl);
+  CU(cudaMemcpyAsync(codes_out, ctx->arena + o_out, N, cudaMemcpyDefault, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->launches = nl;
+  return HB_OK;
+}
+
+// single stages / pipelines on arbitrary bytes (stages.py)
+int hb_stage_encode(hb_ctx* ctx, int stage, int width, const void* in, size_t n, void* out, size_t cap,
+                    size_t* out_len) {
+  if (!ctx || (!in && n) || !out) return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
+  if (stage != HB_PIPE_CR && stage != HB_PIPE_TP && stage != HB_STAGE_HUFFMAN && width != 1 && width != 2 &&
+      width != 4 && width != 8)
+    return set_err(ctx, HB_ESTAGE, "symbol width must be one of (1, 2, 4, 8), got %d", width);
+  cudaSetDevice(ctx->device);
+  const cudaStream_t s = ctx->stream;
+  Layout L;
+  const size_t o_st = L.take(sizeof(DevState));
+  const size_t o_in = L.take(n + 128);
+  const unsigned long long hf_max = 274 + n + 64;
+  const size_t o_hf = L.take(hf_max + 64);
+  const unsigned long long big = 2 * n + 8192;
+  const size_t o_rec = L.take(big);
+  const size_t o_out = L.take(big);
+  size_t c1[9], c2[9];
+  unsigned long long w1, w2;
+  plan_chain(L, big, 8, c1, &w1);
+  plan_chain(L, big, 1, c2, &w2);
+  const unsigned long long lbn = lb_entries(big, 256);
+  const size_t o_lb = L.take(lbn * 8 * 12);
+  int rc = ensure_arena(ctx, L.off);
+  if (rc) return rc;
+  uint8_t* base = ctx->arena;
+  DevState* st = reinterpret_cast<DevState*>(base + o_st);
+  ChainBufs cb1, cb2;
+  std::vector<uint8_t*> t1, t2;
+  bind_chain(base, c1, w1, &cb1, t1);
+  bind_chain(base, c2, w2, &cb2, t2);
+  int nl = 0;
+  CU(cudaMemsetAsync(st, 0, sizeof(DevState), s));
+  CU(cudaMemsetAsync(base + o_lb, 0, lbn * 8 * 12, s));
+  CU(cudaMemcpyAsync(cb1.table, t1.data(), 8 * sizeof(void*), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(cb2.table, t2.data(), 8 * sizeof(void*), cudaMemcpyHostToDevice, s));
+  if (n) CU(cudaMemcpyAsync(base + o_in, in, n, cudaMemcpyDefault, s));
+  k_set_u64<<<1, 1, 0, s>>>(&st->seq_len, n);
+  nl++;
+  unsigned long long* lb = reinterpret_cast<unsigned long long*>(base + o_lb);
+  uint8_t* res = base + o_out;
+  unsigned long long* res_len = &st->stream_len;
+  uint8_t* hf = base + o_hf;
+  auto huff = [&]() {
+    launch_hist(base + o_in, n, st, s, &nl);
+    launch_huffman_build(st, n, hf, s, &nl);
+    launch_huffman_encode(base + o_in, n, hf, lb, st, s, &nl);
+  };
+  switch (stage) {
+    case HB_STAGE_HUFFMAN:
+      huff();
+      res = hf;
+      res_len = &st->hf_rec_len;
+      break;
+    case HB_STAGE_RRE:
+    case HB_STAGE_RZE:
+      launch_reduce_chain_impl(stage, width, SRC_MEM, base + o_in, &st->seq_len, 0, cdiv(n, width) + 1, cb1.rb,
+                               &st->bm[0], res, nullptr, res_len, lb + lbn, lbn, cb1.table, s, &nl);
+      break;
+    case HB_STAGE_TCMS:
+      launch_tcms_encode(base + o_in, &st->seq_len, width, res, res_len, n, s, &nl);
+      break;
+    case HB_STAGE_BIT:
+      launch_bit_encode(base + o_in, &st->seq_len, width, res, res_len, n, s, &nl);
+      break;
+    case HB_PIPE_CR: {
+      huff();
+      uint8_t* rre4 = base + o_rec;
+      launch_reduce_chain_impl(2, 4, SRC_MEM, hf, &st->hf_rec_len, 0, cdiv(hf_max, 4), cb1.rb, &st->bm[0], rre4,
+                               nullptr, &st->scratch[1], lb + lbn, lbn, cb1.table, s, &nl);
+      launch_reduce_chain_impl(3, 1, SRC_TCMS, rre4, &st->scratch[1], 8, big, cb2.rb, &st->bm[1], res, nullptr,
+                               res_len, lb + 5 * lbn, lbn, cb2.table, s, &nl);
+      break;
+    }
+    case HB_PIPE_TP:
+      launch_reduce_chain_impl(2, 1, SRC_TP, base + o_in, &st->seq_len, 0, 10 + cdiv(n + 10, 8) * 8, cb2.rb,
+                               &st->bm[2], res, nullptr, res_len, lb + lbn, lbn, cb2.table, s, &nl);
+      break;
+    default:
+      return set_err(ctx, HB_EARG, "unknown stage %d", stage);
+  }
+  ctx->launches = nl;
+  unsigned long long* hlen = reinterpret_cast<unsigned long long*>(ctx->pinned + 4096);
+  CU(cudaMemcpyAsync(hlen, res_len, 8, cudaMemcpyDeviceToHost, s));
+  HostStatus hs;
+  rc = read_status(ctx, st, &hs);
+  if (rc) return rc;
+  if ((rc = flags_to_code(ctx, hs.flags, hs.detail))) return rc;
+  const unsigned long long rl = *hlen;
+  if (out_len) *out_len = rl;
+  if (rl > cap) return set_err(ctx, HB_EARG, "output capacity %zu < record length %llu", cap, rl);
+  if (rl) CU(cudaMemcpyAsync(out, res, rl, cudaMemcpyDefault, s));
+  CU(cudaStreamSynchronize(s));
+  return HB_OK;
+}
+
+int hb_stage_decode(hb_ctx* ctx, int stage, const void* in, size_t n, void* out, size_t cap, size_t* out_len) {
+  if (!ctx || (!in && n) || !out) return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
+  cudaSetDevice(ctx->device);
+  const cudaStream_t s = ctx->stream;
+  Layout L;
+  const size_t o_st = L.take(sizeof(DevState));
+  const size_t o_in = L.take(n + 128);
+  const unsigned long long capr = cap + 8192;
+  size_t o_tmp[4];
+  unsigned long long wb = capr;
+  for (int k = 0; k < 4; k++) {
+    o_tmp[k] = L.take(wb + 512);
+    wb = cdiv(wb, 8) + 64;
+  }
+  const size_t o_a = L.take(capr + 512), o_b = L.take(capr + 512), o_c = L.take(capr + 512);
+  const size_t o_bmd = L.take(1024);
+  const size_t hd_bytes = huffman_decode_ws_bytes(n + 64);
+  const size_t o_hd = L.take(hd_bytes);
+  const unsigned long long lbn = lb_entries(capr, 256);
+  const size_t o_lb = L.take(lbn * 8 * 12);
+  int rc = ensure_arena(ctx, L.off);
+  if (rc) return rc;
+  uint8_t* base = ctx->arena;
+  DevState* st = reinterpret_cast<DevState*>(base + o_st);
+  uint8_t* tmp[4];
+  for (int k = 0; k < 4; k++) tmp[k] = base + o_tmp[k];
+  uint8_t *ta = base + o_a, *tb = base + o_b, *tc = base + o_c;
+  unsigned long long* lb = reinterpret_cast<unsigned long long*>(base + o_lb);
+  int nl = 0;
+  CU(cudaMemsetAsync(st, 0, sizeof(DevState), s));
+  CU(cudaMemsetAsync(lb, 0, lbn * 8 * 12, s));
+  CU(cudaMemsetAsync(base + o_hd, 0, hd_bytes, s));
+  if (n) CU(cudaMemcpyAsync(base + o_in, in, n, cudaMemcpyDefault, s));
+  k_set_u64<<<1, 1, 0, s>>>(&st->scratch[2], n);
+  nl++;
+  const uint8_t* rec = base + o_in;
+  uint8_t* res = ta;
+  unsigned long long* res_len = &st->scratch[4];
+  switch (stage) {
+    case HB_STAGE_HUFFMAN: {
+      // symbol count from the record header bounds the output
+      if (n < 10) return set_err(ctx, HB_ESTAGE, "truncated stage header");
+      uint64_t nsym = 0;
+      std::vector<uint8_t> h(10);
+      CU(cudaMemcpy(h.data(), in, 10, cudaMemcpyDefault));
+      for (int i = 0; i < 8; i++) nsym |= (uint64_t)h[2 + i] << (8 * i);
+      if (nsym > cap) return set_err(ctx, HB_ESTAGE, "huffman symbol count exceeds capacity");
+      launch_huffman_decode_impl(rec, &st->scratch[2], nsym, capr, n + 64, ta, base + o_hd, lb, st, s, &nl);
+      k_set_u64<<<1, 1, 0, s>>>(res_len, nsym);
+      nl++;
+      break;
+    }
+    case HB_STAGE_RRE:
+    case HB_STAGE_RZE:
+      launch_reduce_decode_impl(stage, rec, &st->scratch[2], capr, ta, res_len, tmp, base + o_bmd, lb, lbn, st, s,
+                                &nl);
+      break;
+    case HB_STAGE_TCMS:
+      launch_tcms_decode(rec, &st->scratch[2], capr, ta, res_len, st, s, &nl);
+      break;
+    case HB_STAGE_BIT:
+      launch_bit_decode(rec, &st->scratch[2], ta, res_len, capr, st, s, &nl);
+      break;
+    case HB_PIPE_CR:
+      launch_reduce_decode_impl(3, rec, &st->scratch[2], capr, ta, &st->scratch[4], tmp, base + o_bmd, lb, lbn, st, s,
+                                &nl);
+      launch_tcms_decode(ta, &st->scratch[4], capr, tb, &st->scratch[5], st, s, &nl);
+      launch_reduce_decode_impl(2, tb, &st->scratch[5], capr, tc, &st->scratch[6], tmp, base + o_bmd, lb + 4 * lbn,
+                                lbn, st, s, &nl);
+      {
+        // symbol count is only known on the device: bound by capacity
+        launch_huffman_decode_impl(tc, &st->scratch[6], ~0ull, capr, capr, ta, base + o_hd, lb + 8 * lbn, st, s, &nl);
+      }
+      res = ta;
+      res_len = &st->hd_nsym;
+      break;
+    case HB_PIPE_TP:
+      launch_reduce_decode_impl(2, rec, &st->scratch[2], capr, ta, &st->scratch[4], tmp, base + o_bmd, lb, lbn, st, s,
+                                &nl);
+      launch_bit_decode(ta, &st->scratch[4], tb, &st->scratch[5], capr, st, s, &nl);
+      launch_tcms_decode(tb, &st->scratch[5], capr, tc, &st->scratch[6], st, s, &nl);
+      res = tc;
+      res_len = &st->scratch[6];
+      break;
+    default:
+      return set_err(ctx, HB_EARG, "unknown stage %d", stage);
+  }
+  ctx->launches = nl;
+  unsigned long long* hlen = reinterpret_cast<unsigned long long*>(ctx->pinned + 4096);
+  CU(cudaMemcpyAsync(hlen, res_len, 8, cudaMemcpyDeviceToHost, s));
+  HostStatus hs;
+  rc = read_status(ctx, st, &hs);
+  if (rc) return rc;
+  if ((rc = flags_to_code(ctx, hs.flags, hs.detail))) return rc;
+  const unsigned long long rl = *hlen;
+  if (out_len) *out_len = rl;
+  if (rl > cap) return set_err(ctx, HB_EARG, "output capacity %zu < decoded length %llu", cap, rl);
+  if (rl) CU(cudaMemcpyAsync(out, res, rl, cudaMemcpyDefault, s));
+  CU(cudaStreamSynchronize(s));
+  return HB_OK;
+}
+
+}  // extern "C"

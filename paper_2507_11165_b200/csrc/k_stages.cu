@@ -1,0 +1,1328 @@
+// k_stages.cu -- the lossless stages of both pipelines on the GPU
+// (stages.py:94-435): bitmap reducers RRE/RZE with <= 3 nested RRE1 bitmaps,
+// TCMS zigzag, BIT bit-plane transpose and canonical Huffman, encode and
+// decode.
+//
+// Every data-dependent size stays on the device (DevState / BmState), so a
+// whole compress or decompress is one asynchronous launch sequence.  Kernels
+// whose work depends on a device-side size are persistent: grid = a few CTAs
+// per SM, tiles handed out by an atomic ticket, and a decoupled look-back
+// (hb_common.cuh) provides each tile's exclusive prefix (kept words, code
+// bits, decoded symbols) in a single pass.
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#include "hb_common.cuh"
+#include "hb_kernels.h"
+
+namespace hb {
+
+constexpr int RD_THREADS = 256;
+constexpr int RD_TILE = RD_THREADS * 32;  // words per tile (8 warps x 32 steps x 32 lanes)
+constexpr unsigned PERSIST_CTAS = 148 * 4;
+
+__device__ __forceinline__ uint64_t ld_bytes(const uint8_t* p, int n) {
+  uint64_t v = 0;
+  for (int i = 0; i < n; i++) v |= (uint64_t)p[i] << (8 * i);
+  return v;
+}
+__device__ __forceinline__ void st_bytes(uint8_t* p, uint64_t v, int n) {
+  for (int i = 0; i < n; i++) p[i] = (uint8_t)(v >> (8 * i));
+}
+__device__ __forceinline__ uint64_t zz(uint64_t u, int w) {  // stages.py:106-107
+  const int top = 8 * w - 1;
+  const uint64_t m = w == 8 ? ~0ull : ((1ull << (8 * w)) - 1);
+  return ((u << 1) ^ (0ull - (u >> top))) & m;
+}
+__device__ __forceinline__ uint64_t unzz(uint64_t u, int w) {  // stages.py:117
+  const uint64_t m = w == 8 ? ~0ull : ((1ull << (8 * w)) - 1);
+  return ((u >> 1) ^ (0ull - (u & 1))) & m;
+}
+// byte-wise zigzag of 8 packed bytes (TCMS w=1, SWAR)
+__device__ __forceinline__ uint64_t zz8x1(uint64_t u) {
+  const uint64_t hi = (u >> 7) & 0x0101010101010101ull;
+  return ((u << 1) & 0xFEFEFEFEFEFEFEFEull) ^ (hi * 0xFFull);
+}
+__device__ __forceinline__ uint64_t unzz8x1(uint64_t u) {
+  const uint64_t lo = u & 0x0101010101010101ull;
+  return ((u >> 1) & 0x7F7F7F7F7F7F7F7Full) ^ (lo * 0xFFull);
+}
+// plane byte k of an 8-byte BIT1 tile held little-endian in g (stages.py:139-140)
+__device__ __forceinline__ uint8_t bit_plane(uint64_t g, int k) {
+  return (uint8_t)((((g >> (7 - k)) & 0x0101010101010101ull) * 0x8040201008040201ull) >> 56);
+}
+
+// ------------------------------------------------------------- sources
+// A reducer source yields little-endian words of `width` bytes of a (virtual)
+// byte record, zero padded past its length.
+
+struct MemSrc {  // plain bytes
+  const uint8_t* p;
+  unsigned long long len;
+  int w;
+  __device__ uint64_t word(unsigned long long i) const {
+    const unsigned long long o = i * w;
+    if (o + w <= len) {
+      if (w == 4 && !((uintptr_t)(p + o) & 3)) return *reinterpret_cast<const uint32_t*>(p + o);
+      if (w == 8 && !((uintptr_t)(p + o) & 7)) return *reinterpret_cast<const uint64_t*>(p + o);
+      return ld_bytes(p + o, w);
+    }
+    uint64_t v = 0;
+    for (int k = 0; k < w; k++)
+      if (o + k < len) v |= (uint64_t)p[o + k] << (8 * k);
+    return v;
+  }
+};
+
+// TCMS(width tw) record of a byte buffer, read as bytes (feeds RZE1 in CR)
+struct TcmsSrc {
+  const uint8_t* p;  // underlying data
+  unsigned long long n;  // underlying length
+  int tw;
+  __device__ uint64_t word(unsigned long long j) const {  // width-1 words
+    if (j < 10) {
+      if (j == 0) return 4;
+      if (j == 1) return (uint64_t)tw;
+      return (n >> (8 * (j - 2))) & 0xFF;
+    }
+    const unsigned long long q = (j - 10) / tw, r = (j - 10) % tw;
+    const unsigned long long o = q * tw;
+    uint64_t u = 0;
+    if (o + tw <= n && tw == 8 && !((uintptr_t)(p + o) & 7))
+      u = *reinterpret_cast<const uint64_t*>(p + o);
+    else
+      for (int k = 0; k < tw; k++)
+        if (o + k < n) u |= (uint64_t)p[o + k] << (8 * k);
+    return (zz(u, tw) >> (8 * r)) & 0xFF;
+  }
+  __device__ unsigned long long len() const { return 10 + cdiv(n, tw) * tw; }
+};
+
+// BIT1(TCMS1(seq)) record bytes (feeds RRE1 in TP): stages.py:430-431
+struct TpSrc {
+  const uint8_t* seq;
+  unsigned long long n;
+  // byte m of the TCMS1 record: header [4,1,n] then zigzag(seq), 0 past end
+  __device__ uint64_t tcms_group(unsigned long long t) const {  // bytes [8t, 8t+8)
+    uint64_t g = 0;
+    if (t <= 1) {
+      for (int k = 0; k < 8; k++) {
+        const unsigned long long m = 8 * t + k;
+        uint64_t b;
+        if (m == 0)
+          b = 4;
+        else if (m == 1)
+          b = 1;
+        else if (m < 10)
+          b = (n >> (8 * (m - 2))) & 0xFF;
+        else
+          b = (m - 10 < n) ? (uint64_t)seq[m - 10] : 0;
+        g |= b << (8 * k);
+      }
+      return t == 1 ? (g & 0xFFFFull) | (zz8x1(g & ~0xFFFFull)) : g;
+    }
+    const unsigned long long o = 8 * t - 10;  // seq offset, o % 8 == 6
+    if (o + 8 <= n) {
+      const uint64_t* w = reinterpret_cast<const uint64_t*>(seq + (o - 6));
+      g = (w[0] >> 48) | (w[1] << 16);
+    } else {
+      for (int k = 0; k < 8; k++)
+        if (o + k < n) g |= (uint64_t)seq[o + k] << (8 * k);
+    }
+    return zz8x1(g);
+  }
+  __device__ uint64_t word(unsigned long long j) const {
+    if (j < 10) {
+      if (j == 0) return 5;
+      if (j == 1) return 1;
+      return ((n + 10) >> (8 * (j - 2))) & 0xFF;
+    }
+    const unsigned long long t = (j - 10) >> 3;
+    return bit_plane(tcms_group(t), (int)((j - 10) & 7));
+  }
+  __device__ unsigned long long len() const { return 10 + cdiv(n + 10, 8) * 8; }
+};
+
+// ------------------------------------------------------- reducer encode
+// stages.py:165-184.  stage 2 = RRE (keep w[i] != w[i-1]), 3 = RZE (w != 0).
+
+template <class Src>
+__device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage, int width, uint8_t* bitmap,
+                             uint8_t* payload, unsigned long long* lb, BmLevel* lv) {
+  __shared__ unsigned long long sh[33];
+  __shared__ unsigned long long tile_sh, base_sh;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned long long ntiles = cdiv(nw, RD_TILE);
+  unsigned long long* ticket = lb;
+  unsigned long long* status = lb + 1;
+  for (;;) {
+    if (threadIdx.x == 0) tile_sh = atomicAdd(ticket, 1ull);
+    __syncthreads();
+    const unsigned long long tile = tile_sh;
+    if (tile >= ntiles) break;
+    const unsigned long long w0 = tile * RD_TILE + (unsigned long long)wid * 1024;
+    uint64_t word[32];
+    uint32_t mask[32];
+    unsigned cnt = 0;
+    uint64_t prev_last = 0;
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+      const unsigned long long i = w0 + k * 32 + lane;
+      const bool in = i < nw;
+      const uint64_t v = in ? src.word(i) : 0;
+      word[k] = v;
+      bool keep;
+      if (stage == 2) {
+        uint64_t pv = __shfl_up_sync(0xffffffffu, v, 1);
+        if (lane == 0) pv = k == 0 ? (i > 0 && i - 1 < nw ? src.word(i - 1) : ~v) : prev_last;
+        keep = in && (i == 0 || v != pv);
+      } else {
+        keep = in && v != 0;
+      }
+      prev_last = __shfl_sync(0xffffffffu, v, 31);
+      const uint32_t m = __ballot_sync(0xffffffffu, keep);
+      mask[k] = m;
+      cnt += __popc(m);
+      if (lane == 0 && w0 + k * 32 < nw) {
+        const uint32_t be = __brev(m);  // word 0 at the MSB (np.packbits order)
+        *reinterpret_cast<uint32_t*>(bitmap + (w0 + k * 32) / 8) = __byte_perm(be, 0, 0x0123);
+      }
+    }
+    unsigned long long total;
+    unsigned long long wex = block_excl_scan<unsigned long long>(lane == 0 ? cnt : 0u, sh, &total);
+    wex = __shfl_sync(0xffffffffu, wex, 0);
+    if (threadIdx.x == 0) base_sh = lookback(status, tile, total);
+    __syncthreads();
+    unsigned long long r = base_sh + wex;
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+      const uint32_t m = mask[k];
+      if ((m >> lane) & 1) {
+        const unsigned long long dst = r + __popc(m & ((1u << lane) - 1));
+        uint8_t* p = payload + dst * width;
+        if (width == 1)
+          *p = (uint8_t)word[k];
+        else if (width == 2)
+          *reinterpret_cast<uint16_t*>(p) = (uint16_t)word[k];
+        else if (width == 4)
+          *reinterpret_cast<uint32_t*>(p) = (uint32_t)word[k];
+        else
+          *reinterpret_cast<uint64_t*>(p) = word[k];
+      }
+      r += __popc(m);
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) lv->kept = base_sh + total;
+    __syncthreads();
+  }
+}
+
+// level 0 of a chain over a typed source
+template <class Src>
+__global__ void __launch_bounds__(RD_THREADS)
+    k_reduce0(Src src, const unsigned long long* len_dev, int stage, int width, BmState* bm, uint8_t* bitmap,
+              uint8_t* payload, unsigned long long* lb) {
+  Src s2 = src;
+  unsigned long long len;
+  if constexpr (sizeof(Src) == sizeof(MemSrc) && __is_same(Src, MemSrc)) {
+    len = *len_dev;
+    s2.len = len;
+  } else if constexpr (__is_same(Src, TcmsSrc)) {
+    s2.n = *len_dev;
+    len = s2.len();
+  } else {
+    s2.n = *len_dev;
+    len = s2.len();
+  }
+  const unsigned long long nw = cdiv(len, (unsigned long long)width);
+  BmLevel* lv = &bm->lv[0];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    lv->orig = len;
+    lv->nwords = nw;
+    lv->bm_len = cdiv(nw, 8);
+    lv->active = 1;
+  }
+  reduce_tiles(s2, nw, stage, width, bitmap, payload, lb, lv);
+}
+
+// nested RRE1 over the previous level's bitmap (stages.py:178-181)
+__global__ void __launch_bounds__(RD_THREADS)
+    k_reduce_nested(int level, BmState* bm, const uint8_t* prev_bitmap, uint8_t* bitmap, uint8_t* payload,
+                    unsigned long long* lb) {
+  const BmLevel* p = &bm->lv[level - 1];
+  if (!p->active || p->bm_len <= 19) return;
+  MemSrc src{prev_bitmap, p->bm_len, 1};
+  const unsigned long long nw = p->bm_len;
+  BmLevel* lv = &bm->lv[level];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    lv->orig = nw;
+    lv->nwords = nw;
+    lv->bm_len = cdiv(nw, 8);
+    lv->active = 1;
+  }
+  reduce_tiles(src, nw, 2, 1, bitmap, payload, lb, lv);
+}
+
+struct ChainLayout {
+  int last;
+  unsigned long long off[4], sec_len[4], pay_off[4], rec_len[4];
+  int flag[4];
+};
+
+__device__ void chain_layout(const BmState* bm, int width0, ChainLayout* L) {
+  int deepest = 0;
+  for (int k = 0; k < 4; k++)
+    if (bm->lv[k].active) deepest = k;
+  for (int k = deepest; k >= 0; k--) {
+    const int w = k == 0 ? width0 : 1;
+    const BmLevel& v = bm->lv[k];
+    bool f = false;
+    if (k < deepest) f = L->rec_len[k + 1] < v.bm_len;
+    L->flag[k] = f;
+    L->sec_len[k] = f ? L->rec_len[k + 1] : v.bm_len;
+    L->rec_len[k] = 19 + L->sec_len[k] + v.kept * w;
+  }
+  L->last = 0;
+  L->off[0] = 0;
+  for (int k = 0; k <= deepest; k++) {
+    L->pay_off[k] = L->off[k] + 19 + L->sec_len[k];
+    if (L->flag[k]) {
+      L->off[k + 1] = L->off[k] + 19;
+    } else {
+      L->last = k;
+      break;
+    }
+  }
+}
+
+// Write the (nested) record: headers, innermost raw bitmap, payloads.
+// dst = out + (dst_off_dev ? *dst_off_dev : 0)
+__global__ void k_chain_assemble(int stage, int width0, BmState* bm, uint8_t* const* bitmaps,
+                                 uint8_t* const* payloads, uint8_t* out, const unsigned long long* dst_off_dev,
+                                 unsigned long long* rec_len_out) {
+  __shared__ ChainLayout L;
+  if (threadIdx.x == 0) chain_layout(bm, width0, &L);
+  __syncthreads();
+  uint8_t* dst = out + (dst_off_dev ? *dst_off_dev : 0ull);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int k = 0; k <= L.last; k++) {
+      uint8_t* h = dst + L.off[k];
+      h[0] = (uint8_t)(k == 0 ? stage : 2);
+      h[1] = (uint8_t)(k == 0 ? width0 : 1);
+      st_bytes(h + 2, bm->lv[k].orig, 8);
+      h[10] = (uint8_t)L.flag[k];
+      st_bytes(h + 11, L.sec_len[k], 8);
+      bm->lv[k].flag = L.flag[k];
+      bm->lv[k].rec_len = L.rec_len[k];
+    }
+    *rec_len_out = L.rec_len[0];
+  }
+  // copy ranges: raw bitmap of the last level, then payloads of levels 0..last
+  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long nth = (unsigned long long)gridDim.x * blockDim.x;
+  {
+    const uint8_t* src = bitmaps[L.last];
+    uint8_t* d = dst + L.off[L.last] + 19;
+    const unsigned long long n = bm->lv[L.last].bm_len;
+    for (unsigned long long i = tid; i < n; i += nth) d[i] = src[i];
+  }
+  for (int k = 0; k <= L.last; k++) {
+    const int w = k == 0 ? width0 : 1;
+    const uint8_t* src = payloads[k];
+    uint8_t* d = dst + L.pay_off[k];
+    const unsigned long long n = bm->lv[k].kept * w;
+    for (unsigned long long i = tid; i < n; i += nth) d[i] = src[i];
+  }
+  // zero pad to the next 8-byte boundary (+8) for word-reading consumers
+  const unsigned long long end = L.rec_len[0];
+  for (unsigned long long i = end + tid; i < ((end + 7) & ~7ull) + 8; i += nth) dst[i] = 0;
+}
+
+struct ChainPtrs {
+  uint8_t* bitmap[4];
+  uint8_t* payload[4];
+};
+
+static unsigned persist_grid(unsigned long long tiles_bound) {
+  return (unsigned)(tiles_bound < PERSIST_CTAS ? (tiles_bound ? tiles_bound : 1) : PERSIST_CTAS);
+}
+
+// Runs level 0 + 3 nested levels + assembly.  lb_ws: 4 zeroed look-back
+// regions of (1 + tiles) u64 each, laid out consecutively with stride lb_stride.
+void launch_reduce_chain_impl(int stage, int width, int src_kind, const uint8_t* src_ptr,
+                              const unsigned long long* len_dev, int tw, unsigned long long max_words,
+                              const ReduceBufs& bufs, BmState* bm, uint8_t* rec_out,
+                              const unsigned long long* dst_off_dev, unsigned long long* rec_len_dev,
+                              unsigned long long* lb_ws, unsigned long long lb_stride, uint8_t* const* dev_ptr_tables,
+                              cudaStream_t s, int* launches) {
+  const unsigned long long tiles0 = cdiv(max_words, RD_TILE);
+  const unsigned g0 = persist_grid(tiles0);
+  switch (src_kind) {
+    case SRC_MEM:
+      k_reduce0<MemSrc><<<g0, RD_THREADS, 0, s>>>(MemSrc{src_ptr, 0, width}, len_dev, stage, width, bm,
+                                                  bufs.bitmap[0], bufs.payload[0], lb_ws);
+      break;
+    case SRC_TCMS:
+      k_reduce0<TcmsSrc><<<g0, RD_THREADS, 0, s>>>(TcmsSrc{src_ptr, 0, tw}, len_dev, stage, width, bm,
+                                                   bufs.bitmap[0], bufs.payload[0], lb_ws);
+      break;
+    default:
+      k_reduce0<TpSrc><<<g0, RD_THREADS, 0, s>>>(TpSrc{src_ptr, 0}, len_dev, stage, width, bm, bufs.bitmap[0],
+                                                 bufs.payload[0], lb_ws);
+      break;
+  }
+  (*launches)++;
+  unsigned long long words = cdiv(max_words, 8);
+  for (int k = 1; k <= 3; k++) {
+    const unsigned g = persist_grid(cdiv(words, RD_TILE));
+    k_reduce_nested<<<g, RD_THREADS, 0, s>>>(k, bm, bufs.bitmap[k - 1], bufs.bitmap[k], bufs.payload[k],
+                                             lb_ws + k * lb_stride);
+    (*launches)++;
+    words = cdiv(words, 8);
+  }
+  k_chain_assemble<<<PERSIST_CTAS, 256, 0, s>>>(stage, width, bm, dev_ptr_tables, dev_ptr_tables + 4, rec_out,
+                                                dst_off_dev, rec_len_dev);
+  (*launches)++;
+}
+
+// ------------------------------------------------------------- Huffman
+// stages.py:246-329.  Code lengths with the heap's (freq, id) order via the
+// equivalent two-queue merge, canonical codes by (len, sym),
+// MSB-first packing.
+
+__global__ void k_hist(const uint8_t* __restrict__ in, unsigned long long n, DevState* st) {
+  __shared__ unsigned h[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    atomicAdd(&h[in[i]], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&st->hist[i], (unsigned long long)h[i]);
+}
+
+void launch_hist(const uint8_t* in, unsigned long long n, DevState* st, cudaStream_t s, int* launches) {
+  unsigned long long b = cdiv(n ? n : 1, 256 * 16);
+  if (b > 148 * 8) b = 148 * 8;
+  k_hist<<<(unsigned)b, 256, 0, s>>>(in, n, st);
+  (*launches)++;
+}
+
+__global__ void __launch_bounds__(256) k_huff_build(DevState* st, unsigned long long n, uint8_t* rec) {
+  __shared__ unsigned long long f[256];
+  __shared__ int sorted[256];
+  __shared__ int parent[512];
+  __shared__ unsigned long long ifreq[256];
+  __shared__ int depth[512];
+  __shared__ uint8_t len[256];
+  __shared__ int np_sh;
+  __shared__ unsigned long long red[33];
+  const int t = threadIdx.x;
+  f[t] = st->hist[t];
+  if (t == 0) np_sh = 0;
+  __syncthreads();
+  if (f[t]) atomicAdd(&np_sh, 1);
+  len[t] = 0;
+  __syncthreads();
+  const int np = np_sh;
+  if (f[t]) {  // rank by (freq, symbol)
+    int r = 0;
+    for (int j = 0; j < 256; j++)
+      if (f[j] && (f[j] < f[t] || (f[j] == f[t] && j < t))) r++;
+    sorted[r] = t;
+  }
+  __syncthreads();
+  if (t == 0) {
+    if (np == 1) {
+      len[sorted[0]] = 1;
+    } else if (np > 1) {
+      int li = 0, ih = 0, it = 0;
+      for (int m = 0; m < np - 1; m++) {
+        int pick[2];
+        unsigned long long pf[2];
+        for (int q = 0; q < 2; q++) {
+          const bool la = li < np, ia = ih < it;
+          // leaf ids (< 256) precede internal ids on equal freq
+          if (la && (!ia || f[sorted[li]] <= ifreq[ih])) {
+            pick[q] = sorted[li];
+            pf[q] = f[sorted[li]];
+            li++;
+          } else {
+            pick[q] = 256 + ih;
+            pf[q] = ifreq[ih];
+            ih++;
+          }
+        }
+        parent[pick[0]] = 256 + m;
+        parent[pick[1]] = 256 + m;
+        ifreq[it++] = pf[0] + pf[1];
+      }
+      const int root = 256 + np - 2;
+      depth[root] = 0;
+      for (int node = root - 1; node >= 256; node--) depth[node] = depth[parent[node]] + 1;
+      for (int sym = 0; sym < 256; sym++)
+        if (f[sym]) len[sym] = (uint8_t)(depth[parent[sym]] + 1);
+    }
+  }
+  __syncthreads();
+  // canonical codes: rank by (len, sym)
+  __shared__ int csorted[256];
+  if (len[t]) {
+    int r = 0;
+    for (int j = 0; j < 256; j++)
+      if (len[j] && (len[j] < len[t] || (len[j] == len[t] && j < t))) r++;
+    csorted[r] = t;
+  }
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long next = 0;
+    int prev = 0;
+    for (int i = 0; i < np; i++) {
+      const int sym = csorted[i];
+      const int L = len[sym];
+      const int sh = L - prev;
+      next = sh >= 64 ? 0 : next << sh;
+      st->hf_code[sym] = next++;
+      prev = L;
+    }
+  }
+  st->hf_len[t] = len[t];
+  // nbits = sum hist * len
+  unsigned long long tot;
+  block_excl_scan<unsigned long long>(f[t] * len[t], red, &tot);
+  if (t == 0) {
+    const unsigned long long nbits = n ? tot : 0;
+    st->hf_nbits = nbits;
+    st->hf_rec_len = 274 + cdiv(nbits, 8);
+    rec[0] = 1;
+    rec[1] = 1;
+    st_bytes(rec + 2, n, 8);
+    st_bytes(rec + 10, nbits, 8);
+    rec[274] = 0;
+    rec[275] = 0;
+  }
+  rec[18 + t] = len[t];
+}
+
+void launch_huffman_build(DevState* st, unsigned long long n, uint8_t* hf_rec, cudaStream_t s, int* launches) {
+  k_huff_build<<<1, 256, 0, s>>>(st, n, hf_rec);
+  (*launches)++;
+}
+
+// zero the payload words [69, end) of the HF record before the OR-packing
+__global__ void k_huff_zero(uint32_t* rec_words, DevState* st) {
+  const unsigned long long end = cdiv(st->hf_rec_len, 4) + 4;
+  for (unsigned long long i = 69 + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < end;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    rec_words[i] = 0;
+}
+
+constexpr int HE_SYMS = 32;  // symbols per thread
+constexpr int HE_TILE = 256 * HE_SYMS;
+
+__device__ __forceinline__ void emit_word(uint32_t* words, unsigned long long wi, uint32_t be, bool owned) {
+  const uint32_t le = __byte_perm(be, 0, 0x0123);
+  if (owned)
+    words[wi] = le;
+  else
+    atomicOr(&words[wi], le);
+}
+
+__global__ void __launch_bounds__(256) k_huff_encode(const uint8_t* __restrict__ in, unsigned long long n,
+                                                     uint32_t* rec_words, unsigned long long* lb, DevState* st) {
+  __shared__ uint8_t slen[256];
+  __shared__ unsigned long long scode[256];
+  __shared__ unsigned long long sh[33];
+  __shared__ unsigned long long tile_sh, base_sh;
+  slen[threadIdx.x] = st->hf_len[threadIdx.x];
+  scode[threadIdx.x] = st->hf_code[threadIdx.x];
+  __syncthreads();
+  const unsigned long long ntiles = cdiv(n, HE_TILE);
+  for (;;) {
+    if (threadIdx.x == 0) tile_sh = atomicAdd(lb, 1ull);
+    __syncthreads();
+    const unsigned long long tile = tile_sh;
+    if (tile >= ntiles) break;
+    const unsigned long long s0 = tile * HE_TILE + (unsigned long long)threadIdx.x * HE_SYMS;
+    uint8_t sym[HE_SYMS];
+    if (s0 + HE_SYMS <= n) {
+      const uint4* p = reinterpret_cast<const uint4*>(in + s0);
+      const uint4 a = p[0], b = p[1];
+      const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int k = 0; k < HE_SYMS; k++) sym[k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+    } else {
+#pragma unroll
+      for (int k = 0; k < HE_SYMS; k++) sym[k] = s0 + k < n ? in[s0 + k] : 0;
+    }
+    unsigned nb = 0;
+#pragma unroll
+    for (int k = 0; k < HE_SYMS; k++) nb += s0 + k < n ? slen[sym[k]] : 0;
+    unsigned long long total;
+    const unsigned long long excl = block_excl_scan<unsigned long long>(nb, sh, &total);
+    if (threadIdx.x == 0) base_sh = lookback(lb + 1, tile, total);
+    __syncthreads();
+    const unsigned long long start = 274ull * 8 + base_sh + excl, end = start + nb;
+    if (nb) {
+      unsigned long long wi = start >> 5;
+      uint64_t acc = 0;
+      int nacc = (int)(start & 31);  // leading bits of the first word belong to others
+      for (int k = 0; k < HE_SYMS; k++) {
+        if (s0 + k >= n) break;
+        int L = slen[sym[k]];
+        const unsigned long long c = scode[sym[k]];
+        while (L > 0) {
+          const int take = L > 32 ? L - 32 : L;  // high part first for codes > 32 bits
+          const uint64_t part = (c >> (L - take)) & ((1ull << take) - 1);
+          acc = (acc << take) | part;
+          nacc += take;
+          L -= take;
+          if (nacc >= 32) {
+            const uint32_t be = (uint32_t)(acc >> (nacc - 32));
+            const bool owned = (wi << 5) >= start && ((wi + 1) << 5) <= end;
+            emit_word(rec_words, wi, be, owned);
+            wi++;
+            nacc -= 32;
+            acc &= nacc ? ((1ull << nacc) - 1) : 0ull;
+          }
+        }
+      }
+      if (nacc > 0) emit_word(rec_words, wi, (uint32_t)(acc << (32 - nacc)), false);
+    }
+    __syncthreads();
+  }
+}
+
+void launch_huffman_encode(const uint8_t* seq, unsigned long long n, uint8_t* hf_rec, unsigned long long* lb_ws,
+                           DevState* st, cudaStream_t s, int* launches) {
+  k_huff_zero<<<PERSIST_CTAS, 256, 0, s>>>(reinterpret_cast<uint32_t*>(hf_rec), st);
+  (*launches)++;
+  if (n == 0) return;
+  const unsigned long long tiles = cdiv(n, HE_TILE);
+  k_huff_encode<<<persist_grid(tiles), 256, 0, s>>>(seq, n, reinterpret_cast<uint32_t*>(hf_rec), lb_ws, st);
+  (*launches)++;
+}
+
+// ------------------------------------------------------ archive tail
+// archive.py:55-74: escape decision, fixed header, counts, stream placement.
+// `base` = 46 + 8 + anchors*prec + 8 (host-known); outliers follow, then the
+// stream length and stream.  The encoded stream was already assembled at
+// stream_off; on escape the raw sequence overwrites it.
+__global__ void k_stream_offset(unsigned long long base, int prec, DevState* st) {
+  st->scratch[0] = base + st->outlier_count * (8ull + prec) + 8;  // stream_off
+}
+
+__global__ void k_archive_tail(uint8_t* arch, unsigned long long base, int prec, const uint8_t* seq,
+                               unsigned long long n, const uint8_t* header46, unsigned long long na, DevState* st) {
+  const unsigned long long soff = st->scratch[0];
+  const unsigned long long enc = st->stream_len;
+  const bool esc = enc > n;
+  const unsigned long long slen = esc ? n : enc;
+  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long nth = (unsigned long long)gridDim.x * blockDim.x;
+  if (esc)
+    for (unsigned long long i = tid; i < n; i += nth) arch[soff + i] = seq[i];
+  if (tid == 0) {
+    for (int i = 0; i < 46; i++) arch[i] = header46[i];
+    arch[9] = esc ? 1 : 0;
+    for (int i = 0; i < 4; i++) arch[10 + i] = st->cfg[i];
+    unsigned long long ebits = (unsigned long long)__double_as_longlong(st->eb);
+    st_bytes(arch + 38, ebits, 8);
+    st_bytes(arch + 46, na, 8);
+    st_bytes(arch + base - 8, st->outlier_count, 8);
+    st_bytes(arch + soff - 8, slen, 8);
+    st->escape = esc;
+    st->archive_len = soff + slen;
+  }
+}
+
+void launch_archive_tail_impl(uint8_t* arch, unsigned long long base, int prec, const uint8_t* seq,
+                              unsigned long long n, const uint8_t* header46, unsigned long long na, DevState* st,
+                              cudaStream_t s, int* launches) {
+  unsigned long long b = cdiv(n, 256 * 8);
+  if (b > PERSIST_CTAS) b = PERSIST_CTAS;
+  k_archive_tail<<<(unsigned)b, 256, 0, s>>>(arch, base, prec, seq, n, header46, na, st);
+  (*launches)++;
+}
+
+void launch_stream_offset(unsigned long long base, int prec, DevState* st, cudaStream_t s, int* launches) {
+  k_stream_offset<<<1, 1, 0, s>>>(base, prec, st);
+  (*launches)++;
+}
+
+// ============================================================= decoders
+
+// Parsed nested reducer record (stages.py:187-221), level 0 outermost.
+struct BmDec {
+  int ok, last;
+  int w[4];
+  unsigned long long orig[4], nsym[4], bm_off[4], bm_len[4], pay_off[4], pay_len[4];
+};
+
+__global__ void k_bm_parse(int stage, const uint8_t* rec, const unsigned long long* len_dev, BmDec* D,
+                           unsigned long long out_cap, unsigned long long* out_len, DevState* st) {
+  D->ok = 0;
+  if (st->flags & (F_STAGE | F_ARCHIVE)) return;
+  unsigned long long off = 0, end = *len_dev;
+  for (int k = 0; k < 4; k++) {
+    const int expect = k == 0 ? stage : 2;
+    if (end - off < 10) return raise_flag(st, F_STAGE, 100);
+    const uint8_t* h = rec + off;
+    if (h[0] != expect) return raise_flag(st, F_STAGE, 101);
+    const int w = h[1];
+    if (w != 1 && w != 2 && w != 4 && w != 8) return raise_flag(st, F_STAGE, 102);
+    const unsigned long long orig = ld_bytes(h + 2, 8);
+    if (end - off < 19) return raise_flag(st, F_STAGE, 103);
+    const int flag = h[10];
+    const unsigned long long bl = ld_bytes(h + 11, 8);
+    if (flag != 0 && flag != 1) return raise_flag(st, F_STAGE, 104);
+    if (bl > end - off - 19) return raise_flag(st, F_STAGE, 105);
+    D->w[k] = w;
+    D->orig[k] = orig;
+    D->nsym[k] = orig / w + (orig % w != 0);
+    D->bm_off[k] = off + 19;
+    D->bm_len[k] = bl;
+    D->pay_off[k] = off + 19 + bl;
+    D->pay_len[k] = end - (off + 19 + bl);
+    if (D->pay_len[k] % w) return raise_flag(st, F_STAGE, 106);
+    if (k > 0 && D->orig[k] != cdiv(D->nsym[k - 1], 8)) return raise_flag(st, F_STAGE, 107);
+    if (!flag) {
+      if (bl != cdiv(D->nsym[k], 8)) return raise_flag(st, F_STAGE, 108);
+      D->last = k;
+      break;
+    }
+    if (k == 3) return raise_flag(st, F_STAGE, 109);  // recursion exceeds maximum depth
+    off = off + 19;
+    end = off + bl;
+  }
+  if (D->orig[0] > out_cap) return raise_flag(st, F_STAGE, 110);
+  for (int k = 1; k <= D->last; k++)
+    if (D->orig[k] > out_cap) return raise_flag(st, F_STAGE, 110);
+  *out_len = D->orig[0];
+  D->ok = 1;
+}
+
+// decode one level: bitmap bits + payload -> words (RRE: kept[cumsum-1], RZE: scatter)
+__global__ void __launch_bounds__(RD_THREADS)
+    k_bm_decode(int stage, int k, const uint8_t* rec, const BmDec* D, const uint8_t* inner_bitmap, uint8_t* out,
+                unsigned long long* lb, DevState* st) {
+  __shared__ unsigned long long sh[33];
+  __shared__ unsigned long long tile_sh, base_sh;
+  if (!D->ok || k > D->last) return;
+  const int w = D->w[k];
+  const int stg = k == 0 ? stage : 2;
+  const unsigned long long nsym = D->nsym[k];
+  const uint8_t* bm = k == D->last ? rec + D->bm_off[k] : inner_bitmap;
+  const uint8_t* pay = rec + D->pay_off[k];
+  const unsigned long long npay = D->pay_len[k] / w;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned long long ntiles = cdiv(nsym, RD_TILE);
+  if (nsym == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && npay != 0) raise_flag(st, F_STAGE, 120);
+    return;
+  }
+  for (;;) {
+    if (threadIdx.x == 0) tile_sh = atomicAdd(lb, 1ull);
+    __syncthreads();
+    const unsigned long long tile = tile_sh;
+    if (tile >= ntiles) break;
+    const unsigned long long w0 = tile * RD_TILE + (unsigned long long)wid * 1024;
+    uint32_t mask[32];
+    unsigned cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 32; j++) {
+      const unsigned long long i0 = w0 + j * 32;  // 32 words = 4 bitmap bytes
+      uint32_t m = 0;
+      if (i0 < nsym) {
+        const unsigned long long bb = i0 >> 3;
+        uint32_t be = 0;
+        for (int q = 0; q < 4; q++) be |= (bb + q < cdiv(nsym, 8) ? (uint32_t)bm[bb + q] : 0u) << (24 - 8 * q);
+        const unsigned long long valid = nsym - i0;
+        if (valid < 32) be &= ~(0xFFFFFFFFu >> valid);
+        m = be;  // bit (31 - l) = word i0 + l
+      }
+      mask[j] = m;
+      cnt += __popc(m);
+    }
+    // mask[] is warp-uniform; one lane's count is the warp's
+    unsigned long long total;
+    unsigned long long wex = block_excl_scan<unsigned long long>(lane == 0 ? cnt : 0u, sh, &total);
+    wex = __shfl_sync(0xffffffffu, wex, 0);
+    if (threadIdx.x == 0) base_sh = lookback(lb + 1, tile, total);
+    __syncthreads();
+    unsigned long long r = base_sh + wex;  // ones before this warp's words
+    if (stg == 2 && tile == 0 && threadIdx.x == 0 && !(mask[0] >> 31)) raise_flag(st, F_STAGE, 121);
+#pragma unroll
+    for (int j = 0; j < 32; j++) {
+      const unsigned long long i = w0 + j * 32 + lane;
+      const uint32_t m = mask[j];
+      if (i < nsym) {
+        const int bit = (m >> (31 - lane)) & 1;
+        const unsigned long long before = r + (lane ? __popc(m >> (32 - lane)) : 0);
+        uint64_t v = 0;
+        if (stg == 2) {
+          const unsigned long long idx = before + bit;  // inclusive count
+          if (idx >= 1 && idx <= npay) v = ld_bytes(pay + (idx - 1) * w, w);
+        } else if (bit && before < npay) {
+          v = ld_bytes(pay + before * w, w);
+        }
+        uint8_t* p = out + i * w;
+        if (w == 1)
+          *p = (uint8_t)v;
+        else
+          st_bytes(p, v, w);
+      }
+      r += __popc(m);
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0 && base_sh + total != npay) raise_flag(st, F_STAGE, 122);
+    __syncthreads();
+  }
+}
+
+void launch_reduce_decode_impl(int stage, const uint8_t* rec, const unsigned long long* rec_len_dev,
+                               unsigned long long out_cap, uint8_t* out, unsigned long long* out_len_dev,
+                               uint8_t* const tmp[4], void* bmdec, unsigned long long* lb_ws,
+                               unsigned long long lb_stride, DevState* st, cudaStream_t s, int* launches) {
+  BmDec* D = reinterpret_cast<BmDec*>(bmdec);
+  k_bm_parse<<<1, 1, 0, s>>>(stage, rec, rec_len_dev, D, out_cap, out_len_dev, st);
+  (*launches)++;
+  // innermost first: level k writes tmp[k] (k >= 1) or out (k == 0)
+  unsigned long long words = out_cap;  // bound on level-0 symbols
+  unsigned long long wb[4];
+  for (int k = 0; k < 4; k++) {
+    wb[k] = words;
+    words = cdiv(words, 8);
+  }
+  for (int k = 3; k >= 0; k--) {
+    const unsigned g = persist_grid(cdiv(wb[k], RD_TILE));
+    k_bm_decode<<<g, RD_THREADS, 0, s>>>(stage, k, rec, D, k < 3 ? tmp[k + 1] : nullptr, k == 0 ? out : tmp[k],
+                                         lb_ws + (3 - k) * lb_stride, st);
+    (*launches)++;
+  }
+}
+
+// TCMS decode (stages.py:111-118), any width, record -> bytes
+__global__ void k_tcms_decode(const uint8_t* rec, const unsigned long long* len_dev, unsigned long long cap,
+                              uint8_t* out, unsigned long long* out_len, DevState* st) {
+  if (st->flags & (F_STAGE | F_ARCHIVE)) return;
+  const unsigned long long n = *len_dev;
+  if (n < 10 || rec[0] != 4) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) raise_flag(st, F_STAGE, 130);
+    return;
+  }
+  const int w = rec[1];
+  const unsigned long long orig = ld_bytes(rec + 2, 8), body = n - 10;
+  if ((w != 1 && w != 2 && w != 4 && w != 8) || body % w || body < orig || body > cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) raise_flag(st, F_STAGE, 131);
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *out_len = orig;
+  const unsigned long long nw = body / w;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nw;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    st_bytes(out + i * w, unzz(ld_bytes(rec + 10 + i * w, w), w), w);
+}
+
+void launch_tcms_decode(const uint8_t* rec, const unsigned long long* rec_len_dev, unsigned long long cap,
+                        uint8_t* out, unsigned long long* out_len_dev, DevState* st, cudaStream_t s, int* launches) {
+  k_tcms_decode<<<PERSIST_CTAS, 256, 0, s>>>(rec, rec_len_dev, cap, out, out_len_dev, st);
+  (*launches)++;
+}
+
+// BIT unshuffle (stages.py:144-160), any width: record -> bytes
+__global__ void k_bit_decode(const uint8_t* rec, const unsigned long long* len_dev, uint8_t* out,
+                             unsigned long long* out_len, unsigned long long cap, DevState* st) {
+  if (st->flags & (F_STAGE | F_ARCHIVE)) return;
+  const unsigned long long n = *len_dev;
+  if (n < 10 || rec[0] != 5) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) raise_flag(st, F_STAGE, 140);
+    return;
+  }
+  const int w = rec[1];
+  const unsigned long long orig = ld_bytes(rec + 2, 8), body = n - 10;
+  const unsigned long long tile = 8ull * w * w;
+  if ((w != 1 && w != 2 && w != 4 && w != 8) || body % tile || body < orig || body > cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) raise_flag(st, F_STAGE, 141);
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *out_len = orig;
+  const int nb = 8 * w;
+  const unsigned long long nwords = body / w;
+  const uint8_t* q = rec + 10;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nwords;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long t = i / nb;
+    const int j = (int)(i % nb);
+    uint64_t u = 0;
+    if (w == 1) {
+      uint64_t g = 0;
+      for (int k = 0; k < 8; k++) g |= (uint64_t)q[t * 8 + k] << (8 * k);
+      u = bit_plane(g, j) ;  // the 8x8 transpose is an involution up to order
+      // bit_plane(g, j) gathers bit (7-j) of each plane byte -> word j
+    } else {
+      for (int k = 0; k < nb; k++)
+        if (q[t * tile + k * w + j / 8] & (0x80 >> (j % 8))) u |= 1ull << (nb - 1 - k);
+    }
+    st_bytes(out + i * w, u, w);
+  }
+}
+
+void launch_bit_decode(const uint8_t* rec, const unsigned long long* len_dev, uint8_t* out,
+                       unsigned long long* out_len_dev, unsigned long long cap, DevState* st, cudaStream_t s,
+                       int* launches) {
+  k_bit_decode<<<PERSIST_CTAS, 256, 0, s>>>(rec, len_dev, out, out_len_dev, cap, st);
+  (*launches)++;
+}
+
+// TCMS / BIT encoders for the single-stage API
+__global__ void k_tcms_encode(const uint8_t* in, const unsigned long long* n_dev, int w, uint8_t* out,
+                              unsigned long long* out_len) {
+  const unsigned long long n = *n_dev, nw = cdiv(n, w);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out[0] = 4;
+    out[1] = (uint8_t)w;
+    st_bytes(out + 2, n, 8);
+    *out_len = 10 + nw * w;
+  }
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nw;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    uint64_t u = 0;
+    for (int k = 0; k < w; k++)
+      if (i * w + k < n) u |= (uint64_t)in[i * w + k] << (8 * k);
+    st_bytes(out + 10 + i * w, zz(u, w), w);
+  }
+}
+
+void launch_tcms_encode(const uint8_t* in, const unsigned long long* n_dev, int width, uint8_t* out,
+                        unsigned long long* out_len_dev, unsigned long long max_n, cudaStream_t s, int* launches) {
+  k_tcms_encode<<<PERSIST_CTAS, 256, 0, s>>>(in, n_dev, width, out, out_len_dev);
+  (*launches)++;
+}
+
+__global__ void k_bit_encode(const uint8_t* in, const unsigned long long* n_dev, int w, uint8_t* out,
+                             unsigned long long* out_len) {
+  const unsigned long long n = *n_dev;
+  const unsigned long long tile = 8ull * w * w, padded = cdiv(n, tile) * tile;
+  const int nb = 8 * w;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out[0] = 5;
+    out[1] = (uint8_t)w;
+    st_bytes(out + 2, n, 8);
+    *out_len = 10 + padded;
+  }
+  // one thread per output plane byte
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < padded;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long t = i / tile;
+    const unsigned long long r = i % tile;
+    const int k = (int)(r / w), jb = (int)(r % w);  // plane k, byte jb of the plane
+    uint8_t b = 0;
+    for (int m = 0; m < 8; m++) {
+      const int j = jb * 8 + m;  // word index within the tile
+      const unsigned long long o = t * tile + (unsigned long long)j * w;
+      uint64_t u = 0;
+      for (int q = 0; q < w; q++)
+        if (o + q < n) u |= (uint64_t)in[o + q] << (8 * q);
+      if ((u >> (nb - 1 - k)) & 1) b |= (uint8_t)(0x80 >> m);
+    }
+    out[10 + i] = b;
+  }
+}
+
+void launch_bit_encode(const uint8_t* in, const unsigned long long* n_dev, int width, uint8_t* out,
+                       unsigned long long* out_len_dev, unsigned long long max_n, cudaStream_t s, int* launches) {
+  k_bit_encode<<<PERSIST_CTAS, 256, 0, s>>>(in, n_dev, width, out, out_len_dev);
+  (*launches)++;
+}
+
+// -------------------------------------------------------- Huffman decode
+// Self-synchronising parallel decode: the payload is cut into S-bit
+// subsequences; each thread decodes from a guessed start until it crosses its
+// subsequence end, then passes re-decode only where a predecessor's end
+// disagrees with the guess (canonical prefix codes resynchronise within a
+// few codewords).  An exclusive scan of per-subsequence symbol counts gives
+// the output offsets for the final decode.
+
+constexpr int HD_S = 1024;       // bits per subsequence
+constexpr int HD_K = 12;         // LUT bits
+constexpr int HD_PASSES = 4;
+
+struct HDTables {
+  int ok;
+  int maxlen, K;
+  unsigned long long nsym, nbits, pay_off, pay_len, nsub;
+  unsigned long long first_code[64];
+  int first_rank[64], count[64];
+  uint8_t syms[256];
+  uint16_t lut[1 << HD_K];  // (len << 8) | sym, 0 = none
+};
+
+struct HDWork {  // per pass: start, end, count per subsequence
+  unsigned long long* s[2];
+  unsigned long long* e[2];
+  unsigned* c[2];
+  unsigned long long* off;
+  int* changed;  // per pass
+};
+
+__global__ void k_hd_setup(const uint8_t* rec, const unsigned long long* len_dev, unsigned long long n_expect,
+                           unsigned long long max_out, HDTables* T, DevState* st) {
+  T->ok = 0;
+  if (st->flags & (F_STAGE | F_ARCHIVE)) return;
+  const unsigned long long n = *len_dev;
+  if (n < 10 || rec[0] != 1) return raise_flag(st, F_STAGE, 150);
+  const int w = rec[1];
+  if (w != 1 && w != 2 && w != 4 && w != 8) return raise_flag(st, F_STAGE, 151);
+  if (w != 1) return raise_flag(st, F_STAGE, 152);
+  if (n < 10 + 8 + 256) return raise_flag(st, F_STAGE, 153);
+  const unsigned long long nsym = ld_bytes(rec + 2, 8), nbits = ld_bytes(rec + 10, 8);
+  const uint8_t* len = rec + 18;
+  const unsigned long long plen = n - 274;
+  if (n_expect != ~0ull && nsym != n_expect) return raise_flag(st, F_ARCHIVE, 159);
+  if (nsym > max_out) return raise_flag(st, F_STAGE, 159);
+  T->nsym = nsym;
+  T->nbits = nbits;
+  T->pay_off = 274;
+  T->pay_len = plen;
+  st->hd_nsym = nsym;
+  if (nsym == 0) {
+    if (nbits || plen) return raise_flag(st, F_STAGE, 154);
+    T->ok = 1;
+    T->nsub = 0;
+    return;
+  }
+  if (nbits / 8 + (nbits % 8 != 0) != plen) return raise_flag(st, F_STAGE, 155);
+  if (nbits == 0) return raise_flag(st, F_STAGE, 155);
+  int cnt[256];
+  for (int L = 0; L < 256; L++) cnt[L] = 0;
+  int ns = 0, maxlen = 0;
+  for (int s = 0; s < 256; s++)
+    if (len[s]) {
+      cnt[len[s]]++;
+      ns++;
+      maxlen = len[s] > maxlen ? len[s] : maxlen;
+    }
+  if (ns == 0) return raise_flag(st, F_STAGE, 156);
+  long long avail = 1;
+  for (int L = 1; L <= maxlen; L++) {
+    avail = avail * 2 - cnt[L];
+    if (avail < 0) return raise_flag(st, F_STAGE, 157);
+    if (avail > 1024) avail = 1024;
+  }
+  if (maxlen > 56) return raise_flag(st, F_UNSUPPORTED, 158);
+  // canonical tables
+  int r = 0;
+  unsigned long long next = 0;
+  int prev = 0;
+  for (int L = 0; L < 64; L++) T->first_rank[L] = -1, T->count[L] = 0, T->first_code[L] = 0;
+  for (int L = 1; L <= maxlen; L++)
+    for (int s = 0; s < 256; s++)
+      if (len[s] == L) {
+        next <<= (L - prev);
+        prev = L;
+        if (T->first_rank[L] < 0) T->first_rank[L] = r, T->first_code[L] = next;
+        T->count[L]++;
+        T->syms[r++] = (uint8_t)s;
+        next++;
+      }
+  const int K = maxlen < HD_K ? maxlen : HD_K;
+  T->maxlen = maxlen;
+  T->K = K;
+  for (int i = 0; i < (1 << HD_K); i++) T->lut[i] = 0;
+  for (int L = 1; L <= K; L++)
+    for (int q = 0; q < T->count[L]; q++) {
+      const unsigned long long code = T->first_code[L] + q;
+      const int sym = T->syms[T->first_rank[L] + q];
+      const unsigned long long lo = code << (K - L), cntk = 1ull << (K - L);
+      for (unsigned long long x = 0; x < cntk; x++) T->lut[lo + x] = (uint16_t)((L << 8) | sym);
+    }
+  T->nsub = cdiv(nbits, HD_S);
+  T->ok = 1;
+}
+
+struct BitReader {
+  const uint8_t* p;
+  unsigned long long nbytes;
+  unsigned long long byte;  // next byte to load
+  uint64_t buf;             // MSB-aligned
+  int nb;
+  __device__ void init(const uint8_t* pay, unsigned long long plen, unsigned long long pos) {
+    p = pay;
+    nbytes = plen;
+    byte = pos >> 3;
+    buf = 0;
+    nb = 0;
+    refill();
+    const int skip = (int)(pos & 7);
+    buf <<= skip;
+    nb -= skip;
+  }
+  __device__ __forceinline__ void refill() {
+    while (nb <= 56) {
+      const uint64_t b = byte < nbytes ? p[byte] : 0;
+      buf |= b << (56 - nb);
+      nb += 8;
+      byte++;
+    }
+  }
+  __device__ __forceinline__ void consume(int L) {
+    buf <<= L;
+    nb -= L;
+    if (nb <= 56) refill();
+  }
+};
+
+// decode from `start` while pos < stop (and < nbits); returns symbols or -1 on error
+__device__ long long hd_decode(const HDTables& T, const uint16_t* lut, const uint8_t* pay, unsigned long long start,
+                               unsigned long long stop, unsigned long long* endp, uint8_t* out, unsigned* zeros) {
+  BitReader br;
+  br.init(pay, T.pay_len, start);
+  unsigned long long pos = start;
+  long long cnt = 0;
+  const unsigned long long nbits = T.nbits;
+  const int K = T.K;
+  while (pos < stop && pos < nbits) {
+    const uint16_t e = lut[br.buf >> (64 - K)];
+    int L, sym;
+    if (e) {
+      L = e >> 8;
+      sym = e & 0xFF;
+    } else {
+      sym = -1;
+      for (L = K + 1; L <= T.maxlen; L++) {
+        if (!T.count[L]) continue;
+        const unsigned long long c = br.buf >> (64 - L);
+        if (c >= T.first_code[L] && c - T.first_code[L] < (unsigned long long)T.count[L]) {
+          sym = T.syms[T.first_rank[L] + (int)(c - T.first_code[L])];
+          break;
+        }
+      }
+      if (sym < 0) {
+        *endp = pos;
+        return -1;
+      }
+    }
+    if (pos + L > nbits) {
+      *endp = pos;
+      return -1;
+    }
+    if (out) {
+      out[cnt] = (uint8_t)sym;
+      if (zeros) *zeros += sym == 0;
+    }
+    pos += L;
+    cnt++;
+    br.consume(L);
+  }
+  *endp = pos;
+  return cnt;
+}
+
+__global__ void __launch_bounds__(256) k_hd_first(const uint8_t* rec, const HDTables* T, HDWork W, DevState* st) {
+  __shared__ uint16_t lut[1 << HD_K];
+  if (!T->ok) return;
+  for (int i = threadIdx.x; i < (1 << HD_K); i++) lut[i] = T->lut[i];
+  __syncthreads();
+  const unsigned long long nsub = T->nsub;
+  const uint8_t* pay = rec + T->pay_off;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nsub;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long s0 = i * HD_S;
+    unsigned long long e;
+    const long long c = hd_decode(*T, lut, pay, s0, s0 + HD_S, &e, nullptr, nullptr);
+    W.s[0][i] = s0;
+    W.e[0][i] = c < 0 ? ~0ull : e;  // error end never matches a successor start
+    W.c[0][i] = c < 0 ? 0u : (unsigned)c;
+  }
+}
+
+// pass p: read buffers (p-1)&1, write p&1
+__global__ void __launch_bounds__(256) k_hd_pass(int p, const uint8_t* rec, const HDTables* T, HDWork W) {
+  __shared__ uint16_t lut[1 << HD_K];
+  if (!T->ok) return;
+  const int rd = (p - 1) & 1, wr = p & 1;
+  const unsigned long long nsub = T->nsub;
+  if (p > 1 && !W.changed[p - 1]) {  // converged: carry the state forward
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nsub;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+      W.s[wr][i] = W.s[rd][i];
+      W.e[wr][i] = W.e[rd][i];
+      W.c[wr][i] = W.c[rd][i];
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < (1 << HD_K); i++) lut[i] = T->lut[i];
+  __syncthreads();
+  const uint8_t* pay = rec + T->pay_off;
+  bool ch = false;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nsub;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long want = i == 0 ? 0ull : W.e[rd][i - 1];
+    if (want == W.s[rd][i] || want == ~0ull) {
+      W.s[wr][i] = W.s[rd][i];
+      W.e[wr][i] = W.e[rd][i];
+      W.c[wr][i] = W.c[rd][i];
+    } else {
+      unsigned long long e;
+      const long long c = want >= (i + 1) * HD_S ? 0 : hd_decode(*T, lut, pay, want, (i + 1) * HD_S, &e, nullptr, nullptr);
+      if (want >= (i + 1) * HD_S) e = want;
+      W.s[wr][i] = want;
+      W.e[wr][i] = c < 0 ? ~0ull : e;
+      W.c[wr][i] = c < 0 ? 0u : (unsigned)c;
+      ch = true;
+    }
+  }
+  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) W.changed[p] = 1;
+}
+
+// exclusive scan of counts (decoupled look-back over 8192-entry tiles)
+__global__ void __launch_bounds__(256) k_hd_scan(const HDTables* T, HDWork W, int fin, unsigned long long* lb,
+                                                 DevState* st) {
+  __shared__ unsigned long long sh[33];
+  __shared__ unsigned long long tile_sh, base_sh;
+  if (!T->ok) return;
+  const unsigned long long nsub = T->nsub;
+  const unsigned long long ntiles = cdiv(nsub, 8192);
+  const unsigned* c = W.c[fin];
+  for (;;) {
+    if (threadIdx.x == 0) tile_sh = atomicAdd(lb, 1ull);
+    __syncthreads();
+    const unsigned long long tile = tile_sh;
+    if (tile >= ntiles) break;
+    const unsigned long long i0 = tile * 8192 + (unsigned long long)threadIdx.x * 32;
+    unsigned long long v[32], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+      v[k] = i0 + k < nsub ? c[i0 + k] : 0;
+      sum += v[k];
+    }
+    unsigned long long total;
+    const unsigned long long ex = block_excl_scan<unsigned long long>(sum, sh, &total);
+    if (threadIdx.x == 0) base_sh = lookback(lb + 1, tile, total);
+    __syncthreads();
+    unsigned long long r = base_sh + ex;
+#pragma unroll
+    for (int k = 0; k < 32; k++)
+      if (i0 + k < nsub) {
+        W.off[i0 + k] = r;
+        r += v[k];
+      }
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+      const unsigned long long tot = base_sh + total;
+      if (tot != T->nsym) raise_flag(st, F_STAGE, 160);
+      if (W.e[fin][nsub - 1] != T->nbits) raise_flag(st, F_STAGE, 161);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_hd_emit(const uint8_t* rec, const HDTables* T, HDWork W, int fin,
+                                                 uint8_t* out, DevState* st) {
+  __shared__ uint16_t lut[1 << HD_K];
+  if (!T->ok) return;
+  if (st->flags & F_STAGE) return;
+  for (int i = threadIdx.x; i < (1 << HD_K); i++) lut[i] = T->lut[i];
+  __syncthreads();
+  const unsigned long long nsub = T->nsub;
+  const uint8_t* pay = rec + T->pay_off;
+  unsigned zeros = 0;
+  bool bad = false;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nsub;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long s0 = W.s[fin][i];
+    const unsigned long long want = i == 0 ? 0ull : W.e[fin][i - 1];
+    if (want != s0 || W.e[fin][i] == ~0ull) {
+      bad = true;
+      continue;
+    }
+    unsigned long long e;
+    const long long c = hd_decode(*T, lut, pay, s0, (i + 1) * HD_S, &e, out + W.off[i], &zeros);
+    bad |= c < 0;
+  }
+  if (zeros) atomicAdd(&st->zero_count, (unsigned long long)zeros);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) raise_flag(st, F_STAGE, 162);
+}
+
+// serial fallback when HD_PASSES did not converge (adversarial streams)
+__global__ void k_hd_serial(const uint8_t* rec, const HDTables* T, HDWork W, int fin) {
+  if (!T->ok || !W.changed[HD_PASSES]) return;
+  const unsigned long long nsub = T->nsub;
+  const uint8_t* pay = rec + T->pay_off;
+  for (unsigned long long i = 1; i < nsub; i++) {
+    const unsigned long long want = W.e[fin][i - 1];
+    if (want == ~0ull) {
+      W.e[fin][i] = ~0ull;
+      continue;
+    }
+    if (want == W.s[fin][i]) continue;
+    unsigned long long e;
+    long long c = want >= (i + 1) * HD_S ? 0 : hd_decode(*T, T->lut, pay, want, (i + 1) * HD_S, &e, nullptr, nullptr);
+    if (want >= (i + 1) * HD_S) e = want;
+    W.s[fin][i] = want;
+    W.e[fin][i] = c < 0 ? ~0ull : e;
+    W.c[fin][i] = c < 0 ? 0u : (unsigned)c;
+  }
+}
+
+size_t huffman_decode_ws_bytes(unsigned long long max_payload_bytes) {
+  const unsigned long long nsub = cdiv(max_payload_bytes * 8, HD_S) + 1;
+  return sizeof(HDTables) + 256 + nsub * (8 * 2 + 8 * 2 + 4 * 2 + 8) + 64 + 256;
+}
+
+void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long* len_dev, unsigned long long n,
+                                unsigned long long max_out, unsigned long long max_payload, uint8_t* seq, void* ws,
+                                unsigned long long* lb_ws, DevState* st, cudaStream_t s, int* launches) {
+  const unsigned long long nsub_max = cdiv(max_payload * 8, HD_S) + 1;
+  uint8_t* p = reinterpret_cast<uint8_t*>(ws);
+  HDTables* T = reinterpret_cast<HDTables*>(p);
+  p += (sizeof(HDTables) + 255) & ~255ull;
+  HDWork W;
+  for (int b = 0; b < 2; b++) {
+    W.s[b] = reinterpret_cast<unsigned long long*>(p);
+    p += nsub_max * 8;
+    W.e[b] = reinterpret_cast<unsigned long long*>(p);
+    p += nsub_max * 8;
+  }
+  W.off = reinterpret_cast<unsigned long long*>(p);
+  p += nsub_max * 8;
+  for (int b = 0; b < 2; b++) {
+    W.c[b] = reinterpret_cast<unsigned*>(p);
+    p += nsub_max * 4;
+  }
+  W.changed = reinterpret_cast<int*>(p);  // HD_PASSES + 1 ints, zeroed by the caller
+  k_hd_setup<<<1, 1, 0, s>>>(hf_rec, len_dev, n, max_out, T, st);
+  (*launches)++;
+  const unsigned g = persist_grid(cdiv(nsub_max, 256));
+  k_hd_first<<<g, 256, 0, s>>>(hf_rec, T, W, st);
+  (*launches)++;
+  for (int pss = 1; pss <= HD_PASSES; pss++) {
+    k_hd_pass<<<g, 256, 0, s>>>(pss, hf_rec, T, W);
+    (*launches)++;
+  }
+  const int fin = HD_PASSES & 1;
+  k_hd_serial<<<1, 1, 0, s>>>(hf_rec, T, W, fin);
+  (*launches)++;
+  k_hd_scan<<<persist_grid(cdiv(nsub_max, 8192)), 256, 0, s>>>(T, W, fin, lb_ws, st);
+  (*launches)++;
+  k_hd_emit<<<g, 256, 0, s>>>(hf_rec, T, W, fin, seq, st);
+  (*launches)++;
+}
+
+// zero count over a sequence (escape / TP paths)
+__global__ void k_count_zeros(const uint8_t* seq, unsigned long long n, DevState* st) {
+  unsigned c = 0;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    c += seq[i] == 0;
+  c = warp_sum<unsigned>(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&st->zero_count, (unsigned long long)c);
+}
+
+void launch_count_zeros(const uint8_t* seq, unsigned long long n, DevState* st, cudaStream_t s, int* launches) {
+  unsigned long long b = cdiv(n ? n : 1, 256 * 16);
+  if (b > PERSIST_CTAS * 2) b = PERSIST_CTAS * 2;
+  k_count_zeros<<<(unsigned)b, 256, 0, s>>>(seq, n, st);
+  (*launches)++;
+}
+
+}  // namespace hb

@@ -1,0 +1,271 @@
+// k_tune.cu -- sampling auto-tuner (tuning.py:66-170) on the GPU.
+//
+// One CTA per (config, sample block): the block's f64 state (17^3 = 39 KB)
+// and its original values live in shared memory; the level's sub-steps run in
+// the reference order, each sub-step's |orig - pred| array is reduced with
+// numpy's pairwise summation (leaves of <= 128 elements with 8 strided
+// accumulators) and accumulated sequentially, exactly like
+// `total += float(np.fabs(ob - pred).sum())` (tuning.py:160).  A 4-thread
+// select kernel then sums block errors with CPython 3.12's Neumaier `sum`
+// (tuning.py:135), takes the (err, index) argmin (:137) and records the
+// winner whose trial grids seed the next level (:140).
+#include <cuda_runtime.h>
+
+#include "hb_common.cuh"
+#include "hb_interp.cuh"
+#include "hb_kernels.h"
+
+namespace hb {
+
+constexpr int TUNE_THREADS = 256;
+// CONFIG_CHOICES (tuning.py:29) as InterpConfig bytes: bit0 linear, bit1 seq1d
+__constant__ uint8_t c_choice[4] = {0x0, 0x2, 0x1, 0x3};
+
+struct SubStep {
+  int start[3], step[3], count[3];
+  int axes[3];
+  int k;
+};
+
+// predictor.py:264-296 on block-local dims
+__device__ int block_steps(const int d[3], int level, bool seq1d, SubStep* out) {
+  const int s = 1 << (level - 1);
+  int n = 0;
+  if (seq1d) {
+    int o[3] = {0, 1, 2};
+    for (int i = 0; i < 3; i++)
+      for (int j = i + 1; j < 3; j++)
+        if (d[o[j]] > d[o[i]] || (d[o[j]] == d[o[i]] && o[j] < o[i])) {
+          int t = o[i];
+          o[i] = o[j];
+          o[j] = t;
+        }
+    for (int k = 0; k < 3; k++) {
+      const int a = o[k];
+      SubStep ss;
+      for (int j = 0; j < 3; j++) {
+        bool earlier = false;
+        for (int m = 0; m < k; m++) earlier |= o[m] == j;
+        ss.start[j] = j == a ? s : 0;
+        ss.step[j] = j == a ? 2 * s : (earlier ? s : 2 * s);
+        ss.count[j] = d[j] > ss.start[j] ? (d[j] - ss.start[j] + ss.step[j] - 1) / ss.step[j] : 0;
+      }
+      ss.axes[0] = a;
+      ss.k = 1;
+      if (ss.count[a] > 0) out[n++] = ss;
+    }
+  } else {
+    const int sets[7] = {1, 2, 4, 3, 5, 6, 7};
+    for (int t = 0; t < 7; t++) {
+      SubStep ss;
+      bool empty = false;
+      ss.k = 0;
+      for (int j = 0; j < 3; j++) {
+        const bool odd = (sets[t] >> j) & 1;
+        ss.start[j] = odd ? s : 0;
+        ss.step[j] = 2 * s;
+        ss.count[j] = d[j] > ss.start[j] ? (d[j] - ss.start[j] + ss.step[j] - 1) / ss.step[j] : 0;
+        if (odd) {
+          if (ss.count[j] == 0) empty = true;
+          ss.axes[ss.k++] = j;
+        }
+      }
+      if (!empty) out[n++] = ss;
+    }
+  }
+  return n;
+}
+
+// numpy pairwise_sum leaf (n <= 128)
+__device__ double pw_leaf(const double* a, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; i++) r = __dadd_rn(r, a[i]);
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) r[j] = a[j];
+  int i;
+  for (i = 8; i < n - (n % 8); i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; i++) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+// enumerate leaves of the pairwise recursion in order (explicit stack)
+__device__ int pw_leaves(int n, int* ls, int* ln) {
+  int stk_s[32], stk_n[32], sp = 0, nl = 0;
+  stk_s[sp] = 0, stk_n[sp] = n, sp++;
+  while (sp) {
+    sp--;
+    const int s0 = stk_s[sp], n0 = stk_n[sp];
+    if (n0 <= 128) {
+      ls[nl] = s0, ln[nl] = n0, nl++;
+    } else {
+      int n2 = n0 / 2;
+      n2 -= n2 % 8;
+      stk_s[sp] = s0 + n2, stk_n[sp] = n0 - n2, sp++;  // right pushed first -> left popped first
+      stk_s[sp] = s0, stk_n[sp] = n2, sp++;
+    }
+  }
+  return nl;
+}
+
+// combine leaf sums along the same recursion (post-order)
+__device__ double pw_combine(int n, const double* leaf, int* cursor) {
+  if (n <= 128) return leaf[(*cursor)++];
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  const double a = pw_combine(n2, leaf, cursor);
+  const double b = pw_combine(n - n2, leaf, cursor);
+  return __dadd_rn(a, b);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TUNE_THREADS)
+    k_tune_level(const T* __restrict__ field, long long fd1, long long fd2, const unsigned long long* origins, int nb,
+                 int b0, int b1, int b2, int top, int level, double* trials, double* berr, DevState* st) {
+  extern __shared__ double tsm[];
+  const int bn = b0 * b1 * b2;
+  double* g = tsm;
+  double* diff = tsm + bn;
+  T* orig = reinterpret_cast<T*>(diff + bn);
+  __shared__ double leaf[160];
+  __shared__ int lstart[160], llen[160];
+  __shared__ int nleaf;
+  const int ci = blockIdx.x / nb, b = blockIdx.x % nb;
+  const unsigned long long ox = origins[3 * b], oy = origins[3 * b + 1], oz = origins[3 * b + 2];
+  // original block values (tuning.py:111-112)
+  for (int i = threadIdx.x; i < bn; i += blockDim.x) {
+    const int z = i % b2, y = (i / b2) % b1, x = i / (b2 * b1);
+    orig[i] = field[((ox + x) * fd1 + oy + y) * fd2 + oz + z];
+  }
+  // state carried from the previous level's winner (tuning.py:140)
+  const size_t set_stride = (size_t)4 * nb * bn;
+  if (level == top) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < bn; i += blockDim.x) g[i] = (double)orig[i];
+  } else {
+    const int w = st->tune_winner[level];  // winner of level+1
+    const double* src = trials + (size_t)((level + 1) & 1) * set_stride + ((size_t)w * nb + b) * bn;
+    for (int i = threadIdx.x; i < bn; i += blockDim.x) g[i] = src[i];
+  }
+  __syncthreads();
+  const uint8_t cb = c_choice[ci];
+  const bool linear = cb & 1, seq1d = (cb >> 1) & 1;
+  const double eb = st->eb, two_eb = st->two_eb;
+  const int dims[3] = {b0, b1, b2};
+  SubStep ss[7];
+  const int nss = block_steps(dims, level, seq1d, ss);
+  const int s = 1 << (level - 1);
+  double total = 0.0;
+  for (int t = 0; t < nss; t++) {
+    const SubStep& S = ss[t];
+    const int n = S.count[0] * S.count[1] * S.count[2];
+    for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+      int c[3];
+      c[2] = S.start[2] + (idx % S.count[2]) * S.step[2];
+      c[1] = S.start[1] + ((idx / S.count[2]) % S.count[1]) * S.step[1];
+      c[0] = S.start[0] + (idx / (S.count[2] * S.count[1])) * S.step[0];
+      const int lin = (c[0] * b1 + c[1]) * b2 + c[2];
+      double pv[3];
+      int ov[3];
+      for (int i = 0; i < S.k; i++) {
+        const int a = S.axes[i];
+        const int stp = (a == 0 ? b1 * b2 : (a == 1 ? b2 : 1)) * s;
+        const int cls = classify(c[a], dims[a], s, linear);
+        // samples at -3s, -1s, +1s, +3s; only in-range ones are used by cls
+        const double v0 = c[a] >= 3 * s ? g[lin - 3 * stp] : 0.0;
+        const double v1 = g[lin - stp];
+        const double v2 = c[a] + s < dims[a] ? g[lin + stp] : 0.0;
+        const double v3 = c[a] + 3 * s < dims[a] ? g[lin + 3 * stp] : 0.0;
+        pv[i] = apply_stencil(cls, v0, v1, v2, v3);
+        ov[i] = stencil_order(cls);
+      }
+      const double pred = S.k == 1 ? pv[0] : combine_axes(S.k, pv, ov);
+      const double o = (double)orig[lin];
+      diff[idx] = fabs(__dsub_rn(o, pred));
+      double r;
+      quantize<sizeof(T) == 4>(o, pred, eb, two_eb, &r);
+      g[lin] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) nleaf = pw_leaves(n, lstart, llen);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nleaf; i += blockDim.x) leaf[i] = pw_leaf(diff + lstart[i], llen[i]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int cur = 0;
+      total = __dadd_rn(total, pw_combine(n, leaf, &cur));
+    }
+    __syncthreads();
+  }
+  double* dst = trials + (size_t)(level & 1) * set_stride + ((size_t)ci * nb + b) * bn;
+  for (int i = threadIdx.x; i < bn; i += blockDim.x) dst[i] = g[i];
+  if (threadIdx.x == 0) berr[ci * nb + b] = total;
+}
+
+// tuning.py:135-140
+__global__ void k_tune_select(int nb, int level, const double* berr, DevState* st) {
+  __shared__ double e[4];
+  const int ci = threadIdx.x;
+  if (ci < 4) {
+    const double* x = berr + ci * nb;
+    double f = __dadd_rn(0.0, x[0]), c = 0.0;  // sum() starts from int 0
+    for (int i = 1; i < nb; i++) {
+      const double t = __dadd_rn(f, x[i]);
+      if (fabs(f) >= fabs(x[i]))
+        c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x[i]));
+      else
+        c = __dadd_rn(c, __dadd_rn(__dsub_rn(x[i], t), f));
+      f = t;
+    }
+    if (c != 0.0 && isfinite(c)) f = __dadd_rn(f, c);
+    e[ci] = f;
+    st->tune_errs[(level - 1) * 4 + ci] = f;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int best = 0;
+    for (int i = 1; i < 4; i++)
+      if (e[i] < e[best]) best = i;
+    st->tune_winner[level - 1] = best;
+    st->cfg[level - 1] = c_choice[best];
+  }
+}
+
+static size_t tune_smem(const TunePlan& p, int prec) {
+  return (size_t)p.bn * 8 * 2 + (size_t)p.bn * prec;
+}
+
+bool tune_supported(const TunePlan& p) { return tune_smem(p, 8) <= 200 * 1024; }
+
+void launch_tune_level(const TunePlan& p, const void* field, int prec, const uint64_t dims[3],
+                       const unsigned long long* origins, int level, double* trials, double* berr, DevState* st,
+                       cudaStream_t s, int* launches) {
+  const size_t smem = tune_smem(p, prec);
+  if (prec == 4) {
+    cudaFuncSetAttribute(k_tune_level<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_tune_level<float><<<4 * p.nb, TUNE_THREADS, smem, s>>>((const float*)field, dims[1], dims[2], origins, p.nb,
+                                                             p.shape[0], p.shape[1], p.shape[2], p.top, level, trials,
+                                                             berr, st);
+  } else {
+    cudaFuncSetAttribute(k_tune_level<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_tune_level<double><<<4 * p.nb, TUNE_THREADS, smem, s>>>((const double*)field, dims[1], dims[2], origins, p.nb,
+                                                              p.shape[0], p.shape[1], p.shape[2], p.top, level,
+                                                              trials, berr, st);
+  }
+  (*launches)++;
+}
+
+void launch_tune_select(const TunePlan& p, int level, const double* berr, DevState* st, cudaStream_t s,
+                        int* launches) {
+  k_tune_select<<<1, 32, 0, s>>>(p.nb, level, berr, st);
+  (*launches)++;
+}
+
+}  // namespace hb

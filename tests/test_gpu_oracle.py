@@ -1,0 +1,59 @@
+"""GPU vs the pinned CPU oracle on seeded inputs larger than the goldens,
+plus size-independent properties at the benchmark size (512^3)."""
+import numpy as np
+import pytest
+
+from conftest import has_cuda
+
+pytestmark = pytest.mark.gpu
+
+if not has_cuda():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2507_11165_b200 as hb  # noqa: E402
+from paper_2507_11165_b200 import synth  # noqa: E402
+
+
+CASES = [
+    ("grf", (96, 80, 112), "rel", 1e-3, "f32"),
+    ("grf", (130, 66, 97), "rel", 1e-4, "f32"),
+    ("gauss", (128, 128, 128), "rel", 1e-3, "f32"),
+    ("rough", (64, 96, 80), "rel", 1e-3, "f32"),
+    ("rough", (50, 120, 110), "rel", 1e-2, "f64"),
+    ("grf", (600, 900), "rel", 1e-3, "f32"),
+    ("rough", (333, 777), "rel", 1e-5, "f32"),
+    ("grf", (256, 384, 20), "abs", 2e-3, "f32"),
+]
+
+
+@pytest.mark.parametrize("kind,dims,ebm,mag,dt", CASES)
+def test_archive_matches_oracle(oracle, kind, dims, ebm, mag, dt):
+    vals = synth.make(kind, dims, seed=11, dtype=dt)
+    f = hb.Field(vals, ndim=len(dims))
+    spec = hb.ErrorBoundSpec(ebm, mag)
+    for mode in ("cr", "tp"):
+        blob = hb.compress(f, spec, mode)
+        ref = oracle.compress(vals, ebm, mag, mode, len(dims))
+        assert len(blob) == len(ref), (kind, dims, mode)
+        assert blob == ref, (kind, dims, mode)
+        out = hb.decompress(blob)
+        back, _ = oracle.decompress(blob)
+        assert np.array_equal(out.values, back.reshape(out.values.shape))
+        eb = oracle.resolve_eb(vals, ebm, mag)
+        assert np.max(np.abs(out.values.astype(np.float64) - f.values.astype(np.float64))) <= eb
+
+
+def test_512_cubed_properties():
+    import torch
+    vals = synth.make_device("grf", (512, 512, 512), seed=2025)
+    f = hb.Field(vals)
+    spec = hb.ErrorBoundSpec("rel", 1e-3)
+    a_cr = hb.compress_device(f, spec, "cr").clone()
+    a_tp = hb.compress_device(f, spec, "tp").clone()
+    assert torch.equal(hb.compress_device(f, spec, "cr"), a_cr)  # deterministic
+    info = hb.section_sizes(a_cr.cpu().numpy().tobytes())
+    r_cr = hb.decompress_device(a_cr, f.dims, np.float32)
+    r_tp = hb.decompress_device(a_tp, f.dims, np.float32)
+    assert torch.equal(r_cr.values, r_tp.values)  # CR/TP reconstructions identical
+    err = (r_cr.values.double() - vals.double()).abs().max().item()
+    assert err <= info["abs_eb"]

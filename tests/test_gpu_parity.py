@@ -1,0 +1,113 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+golden outputs (tests/golden/) and against the pinned CPU oracle on larger
+seeded inputs.  Bit-exact for codes, outliers, stage records and archives;
+decompressed values bit-identical to the reference's and within eb."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, case_names, cfg_case_names, has_cuda, load_case
+
+pytestmark = pytest.mark.gpu
+
+if not has_cuda():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2507_11165_b200 as hb  # noqa: E402
+
+
+def sha(b):
+    return hashlib.sha256(b).hexdigest()
+
+
+def field_of(c):
+    return hb.Field(np.ascontiguousarray(c["input"]), ndim=int(c["ndim"]))
+
+
+@pytest.mark.parametrize("name", case_names())
+def test_compress_matches_reference_archive(name):
+    c = load_case(name)
+    f = field_of(c)
+    spec = hb.ErrorBoundSpec(str(c["eb_mode"]), float(c["mag"]))
+    for mode, key in (("cr", "arch_cr"), ("tp", "arch_tp")):
+        blob = hb.compress(f, spec, mode)
+        ref = c[key].tobytes()
+        assert len(blob) == len(ref), (name, mode)
+        assert blob == ref, (name, mode)
+
+
+@pytest.mark.parametrize("name", case_names())
+def test_decompress_reference_archive(name):
+    c = load_case(name)
+    for key in ("arch_cr", "arch_tp"):
+        out = hb.decompress(c[key].tobytes())
+        assert out.ndim == int(c["ndim"])
+        assert out.dtype == c["input"].dtype
+        assert sha(out.values.tobytes()) == str(c["recon_sha256"]), (name, key)
+        err = np.max(np.abs(out.values.astype(np.float64) - c["input"].astype(np.float64)))
+        assert err <= float(c["eb"])
+
+
+@pytest.mark.parametrize("name", case_names())
+def test_tune_report_matches(name):
+    c = load_case(name)
+    f = field_of(c)
+    rep = hb.tune_report(f, float(c["eb"]))
+    assert rep.chosen.to_bytes() == bytes(c["cfg"])
+    ge = c["tune_errs"]
+    for level, errs in rep.level_errors.items():
+        for i, cfg in enumerate(hb.tuning.CONFIG_CHOICES):
+            assert errs[cfg] == ge[level - 1, i], (name, level, cfg)
+
+
+@pytest.mark.parametrize("name", case_names())
+def test_decompose_outliers_and_seq(name):
+    c = load_case(name)
+    f = field_of(c)
+    qf = hb.decompose(f, float(c["eb"]), hb.InterpConfig.from_bytes(bytes(c["cfg"])))
+    assert np.array_equal(qf.outlier_indices, c["oidx"])
+    assert np.array_equal(qf.outlier_values, c["oval"])
+    assert np.array_equal(qf.anchors.values, c["anchors"])
+    lm = hb.LevelMap(f.dims, qf.anchors.stride)
+    assert np.array_equal(hb.reorder(qf.codes, lm), c["seq"])
+
+
+@pytest.mark.parametrize("name", cfg_case_names())
+def test_decompose_reconstruct_every_config(name):
+    with np.load(os.path.join(GOLDEN, f"cfg_{name}.npz")) as z:
+        c = {k: z[k] for k in z.files}
+    f = hb.Field(np.ascontiguousarray(c["input"]), ndim=int(c["ndim"]))
+    eb = float(c["eb"])
+    for k in range(5):
+        cfg = hb.InterpConfig.from_bytes(bytes(c[f"cfg{k}"]))
+        qf = hb.decompose(f, eb, cfg)
+        assert np.array_equal(qf.codes, c[f"codes{k}"]), (name, k)
+        assert np.array_equal(qf.outlier_indices, c[f"oidx{k}"])
+        assert np.array_equal(qf.outlier_values, c[f"oval{k}"])
+        rec = hb.reconstruct(qf, eb, cfg, dims=f.dims, ndim=f.ndim)
+        assert sha(rec.values.tobytes()) == str(c[f"recon_sha256_{k}"]), (name, k)
+
+
+def test_stage_records():
+    with np.load(os.path.join(GOLDEN, "stages.npz")) as z:
+        c = {k: z[k] for k in z.files}
+    st = hb.stages
+    for i in range(int(c["count"])):
+        data = c[f"in{i}"].tobytes()
+        assert st.huffman_encode(data) == c[f"hf{i}"].tobytes(), i
+        assert st.huffman_decode(c[f"hf{i}"].tobytes()) == data, i
+        assert st.pipeline_cr_encode(data) == c[f"cr{i}"].tobytes(), i
+        assert st.pipeline_tp_encode(data) == c[f"tp{i}"].tobytes(), i
+        assert st.pipeline_cr_decode(c[f"cr{i}"].tobytes()) == data, i
+        assert st.pipeline_tp_decode(c[f"tp{i}"].tobytes()) == data, i
+        for w in (1, 2, 4, 8):
+            assert st.tcms_encode(data, w) == c[f"tcms{w}_{i}"].tobytes(), (i, w)
+            assert st.tcms_decode(c[f"tcms{w}_{i}"].tobytes()) == data
+            assert st.bit_shuffle(data, w) == c[f"bit{w}_{i}"].tobytes(), (i, w)
+            assert st.bit_unshuffle(c[f"bit{w}_{i}"].tobytes()) == data
+            assert st.rre_encode(data, w) == c[f"rre{w}_{i}"].tobytes(), (i, w)
+            assert st.rre_decode(c[f"rre{w}_{i}"].tobytes()) == data
+            assert st.rze_encode(data, w) == c[f"rze{w}_{i}"].tobytes(), (i, w)
+            assert st.rze_decode(c[f"rze{w}_{i}"].tobytes()) == data
