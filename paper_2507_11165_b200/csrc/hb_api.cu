@@ -1002,7 +1002,7 @@ int hb_stage_encode(hb_ctx* ctx, int stage, int width, const void* in, size_t n,
   const size_t o_out = L.take(big);
   size_t c1[9], c2[9];
   unsigned long long w1, w2;
-  plan_chain(L, big, 8, c1, &w1);
+  plan_chain(L, big, 1, c1, &w1);  // width 1 = most words: fits every stage width
   plan_chain(L, big, 1, c2, &w2);
   const unsigned long long lbn = lb_entries(big, 256);
   const size_t o_lb = L.take(lbn * 8 * 12);

@@ -144,9 +144,16 @@ __global__ void k_finish_eb(DevState* st, int eb_mode, double mag) {
   st->two_eb = __dmul_rn(2.0, eb);
 }
 
+__global__ void k_minmax_init(DevState* st) {
+  st->vmin_bits = ~0ull;
+  st->vmax_bits = 0ull;
+}
+
 void launch_minmax(const void* field, int prec, unsigned long long n, DevState* st, int eb_mode, double mag,
                    cudaStream_t s, int* launches) {
   if (eb_mode == 1) {
+    k_minmax_init<<<1, 1, 0, s>>>(st);
+    (*launches)++;
     unsigned long long blocks = cdiv(n, 256ull * 4);
     if (blocks > 148ull * 16) blocks = 148ull * 16;
     if (prec == 4)

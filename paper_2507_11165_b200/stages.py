@@ -139,8 +139,8 @@ def pipeline_cr_encode(data: bytes) -> bytes:
 
 
 def pipeline_cr_decode(blob: bytes) -> bytes:
-    # symbols <= Huffman bits <= 8 x (every intermediate record) <= 8 x the RZE orig_len
-    return _decode(_PIPE_CR, blob, 8 * _bitmap_cap(blob))
+    # stage by stage so every output buffer is sized from its record header
+    return huffman_decode(rre_decode(tcms_decode(rze_decode(blob))))
 
 
 def pipeline_tp_encode(data: bytes) -> bytes:
@@ -148,4 +148,4 @@ def pipeline_tp_encode(data: bytes) -> bytes:
 
 
 def pipeline_tp_decode(blob: bytes) -> bytes:
-    return _decode(_PIPE_TP, blob, _bitmap_cap(blob))
+    return tcms_decode(bit_unshuffle(rre_decode(blob)))
