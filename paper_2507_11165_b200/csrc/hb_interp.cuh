@@ -85,6 +85,35 @@ __device__ __forceinline__ int quantize(double o, double p, double eb, double tw
   return ok ? (int)__dadd_rn(q, 128.0) : 0;
 }
 
+// Same result as quantize<>, with the IEEE quotient |err|/two_eb replaced by a
+// multiplication with the rounded reciprocal whenever that cannot change
+// floor(q + 0.5).  For x = |err|/two_eb < 200 the product differs from the
+// correctly rounded quotient by < 2^-43 after the +0.5, so a fractional part
+// at least 2^-40 away from an integer proves both floors agree; otherwise
+// (or for non-finite values) the exact division is evaluated.  For x >= 200
+// the code is an outlier either way (|q| > 127) and the stored value is the
+// original, so an off-by-one q cannot change the result.
+template <bool CAST32>
+__device__ __forceinline__ int quantize_fast(double o, double p, double eb, double two_eb, double inv_two_eb,
+                                             double* recon) {
+  const double err = __dsub_rn(o, p);
+  const double ae = fabs(err);
+  double u = __dadd_rn(__dmul_rn(ae, inv_two_eb), 0.5);
+  double f = floor(u);
+  const double fr = __dsub_rn(u, f);
+  if (!(fr > 0x1p-40 && fr < 1.0 - 0x1p-40) && !(u >= 200.5)) {  // NaN lands here too
+    u = __dadd_rn(__ddiv_rn(ae, two_eb), 0.5);
+    f = floor(u);
+  }
+  const double q = copysign(f, err);
+  const bool small = fabs(q) <= 127.0;
+  const double r = __dadd_rn(p, __dmul_rn(two_eb, q));
+  const double stored = CAST32 ? (double)__double2float_rn(r) : r;
+  const bool ok = small && (fabs(__dsub_rn(o, stored)) <= eb);
+  *recon = ok ? r : o;
+  return ok ? (int)__dadd_rn(q, 128.0) : 0;
+}
+
 // predictor.py:399: replay of a stored code
 __device__ __forceinline__ double dequantize(double p, double two_eb, int code) {
   return __dadd_rn(p, __dmul_rn(two_eb, __dsub_rn((double)code, 128.0)));

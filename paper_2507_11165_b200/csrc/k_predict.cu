@@ -18,6 +18,7 @@
 // level reads.
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "hb_common.cuh"
 #include "hb_interp.cuh"
@@ -515,6 +516,9 @@ void level_kernel_smem_init() {
 
 void launch_level_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq, uint32_t* obm,
                            DevState* st, cudaStream_t s, int* launches) {
+  (*launches)++;
+  if (!getenv("HB_GENERIC_LEVELS") && launch_level_tiled_compress(g, field, prec, E, seq, obm, st, s)) return;
+  (*launches)--;
   level_kernel_smem_init();
   const unsigned blocks = (unsigned)((long long)g.ntile[0] * g.ntile[1] * g.ntile[2]);
   const size_t smem = (size_t)g.smem_doubles * sizeof(double);
@@ -530,6 +534,11 @@ void launch_level_compress(const LevelGeom& g, const void* field, int prec, doub
 void launch_level_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
                              const unsigned long long* ocount_dev, double* E, void* out, int prec, DevState* st,
                              cudaStream_t s, int* launches) {
+  (*launches)++;
+  if (!getenv("HB_GENERIC_LEVELS") &&
+      launch_level_tiled_decompress(g, seq, oidx, oval, ocount_dev, E, out, prec, st, s))
+    return;
+  (*launches)--;
   level_kernel_smem_init();
   const unsigned blocks = (unsigned)((long long)g.ntile[0] * g.ntile[1] * g.ntile[2]);
   const size_t smem = (size_t)g.smem_doubles * sizeof(double);
