@@ -53,12 +53,30 @@ def _compress_into(field: Field, spec: ErrorBoundSpec, mode: str, out, cap: int)
     return olen.value, eb.value, bytes(cfg)
 
 
+_PINNED = {"buf": None}
+
+
+def _pinned(cap: int):
+    """Reusable page-locked staging buffer for archive read-back."""
+    b = _PINNED["buf"]
+    if b is None or b.size < cap:
+        try:
+            import torch
+            t = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+            _PINNED["tensor"] = t
+            b = t.numpy()
+        except Exception:
+            b = np.empty(cap, np.uint8)
+        _PINNED["buf"] = b
+    return b
+
+
 def compress(field: Field, spec: ErrorBoundSpec, mode: str = MODE_CR) -> bytes:
     """Compress a field under the given error bound; returns archive bytes."""
     if mode not in _MODE_BYTE:
         raise ValueError(f"mode must be {MODE_CR!r} or {MODE_TP!r}, got {mode!r}")
     cap = compress_bound(field.dims, _prec(field))
-    out = np.empty(cap, np.uint8)
+    out = _pinned(cap)
     n, _, _ = _compress_into(field, spec, mode, out, cap)
     return out[:n].tobytes()
 
@@ -109,7 +127,7 @@ def decompress(blob, out=None) -> Field:
     c = _lib.ctx()
     rc = L.hb_decompress(c, _lib.ptr(arr), len(data), _lib.ptr(out), out.nbytes, None)
     _lib.raise_for(rc, c)
-    return Field(out, ndim=info.ndim)
+    return Field._trusted(out, info.ndim)
 
 
 def decompress_device(archive, dims, dtype, ndim: int = 3, out=None):
@@ -121,7 +139,7 @@ def decompress_device(archive, dims, dtype, ndim: int = 3, out=None):
     L, c = _lib.lib(), _lib.ctx()
     rc = L.hb_decompress(c, _lib.ptr(archive), archive.numel(), _lib.ptr(out), out.numel() * out.element_size(), None)
     _lib.raise_for(rc, c)
-    return Field(out, ndim=ndim)
+    return Field._trusted(out, ndim)
 
 
 def section_sizes(blob: bytes) -> dict:

@@ -774,7 +774,7 @@ int hb_decompress(hb_ctx* ctx, const void* archive, size_t len, void* field_out,
   ctx->mark("decode_stream");
   // reconstruct (predictor.py:378-416) with fused inverse reorder
   if (top == 0) {
-    launch_copy_anchors_out(arch + I.anchor_off, prec, N, out, s, &nl);
+    launch_copy_anchors_out(arch + I.anchor_off, prec, N, out, st, s, &nl);
   } else {
     launch_anchor_load(arch + I.anchor_off, prec, I.dims, A, E, s, &nl);
     for (int level = top; level >= 1; level--) {
@@ -926,7 +926,7 @@ int hb_reconstruct(hb_ctx* ctx, const uint8_t* seq_in, const uint64_t* oidx_in, 
   }
   void* out = mem_kind(field_out) == MEM_HOST ? (void*)(base + o_out) : field_out;
   if (top == 0) {
-    launch_copy_anchors_out(base + o_anc, prec, N, out, s, &nl);
+    launch_copy_anchors_out(base + o_anc, prec, N, out, st, s, &nl);
   } else {
     launch_anchor_load(base + o_anc, prec, dims, A, reinterpret_cast<double*>(base + o_E), s, &nl);
     for (int level = top; level >= 1; level--) {

@@ -150,6 +150,44 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* statu
   return excl;
 }
 
+// Warp-parallel variant: called by all 32 lanes of ONE warp of tile `t`;
+// inspects 32 predecessors per round (one status word per lane), so the walk
+// costs ~t/32 L2 round trips even when no predecessor has its inclusive
+// prefix yet.  Returns the exclusive prefix on every lane.
+__device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* status, unsigned long long t,
+                                                            unsigned long long agg) {
+  const int lane = threadIdx.x & 31;
+  if (t == 0) {
+    if (lane == 0) {
+      __threadfence();
+      atomicExch(&status[0], LB_INC | agg);
+    }
+    return 0;
+  }
+  if (lane == 0) atomicExch(&status[t], LB_AGG | agg);
+  unsigned long long excl = 0;
+  long long base = (long long)t - 1;
+  while (true) {
+    const long long j = base - lane;
+    unsigned long long s = j >= 0 ? ld_volatile(&status[j]) : LB_INC;
+    while (__any_sync(0xffffffffu, (s >> 62) == 0))
+      if ((s >> 62) == 0) s = ld_volatile(&status[j]);
+    const unsigned inc = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+    if (inc) {
+      const int first = __ffs(inc) - 1;
+      excl += warp_sum<unsigned long long>(lane <= first ? (s & LB_MASK) : 0ull);
+      break;
+    }
+    excl += warp_sum<unsigned long long>(s & LB_MASK);
+    base -= 32;
+  }
+  if (lane == 0) {
+    __threadfence();
+    atomicExch(&status[t], LB_INC | (excl + agg));
+  }
+  return excl;
+}
+
 // ordered encodings for float min/max atomics
 __device__ __forceinline__ unsigned long long ord_bits(double v) {
   unsigned long long b = (unsigned long long)__double_as_longlong(v);

@@ -27,6 +27,10 @@ struct LevelGeom {
   int smem_doubles;
   // LevelMap closed form (ordering.py:68-84) at ordering level L-1
   long long prefix;  // points at coarser ordering levels
+  // affine address steps per unit of half-index (kernel-parameter constants)
+  long long kl[3];   // field element index
+  long long ke[3];   // even-lattice E index
+  long long ks0, ks1_odd0, ks1_even0, eyez, ez;  // Eq. 3 slot
 };
 
 void make_level_geom(const uint64_t dims[3], int level, LevelGeom* g);
@@ -51,8 +55,8 @@ void launch_anchor_load(const uint8_t* anchors /*byte addressed*/, int prec, con
 void launch_level_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
                              const unsigned long long* ocount_dev, double* E, void* out, int prec, DevState* st,
                              cudaStream_t s, int* launches);
-void launch_copy_anchors_out(const uint8_t* anchors, int prec, unsigned long long n, void* out, cudaStream_t s,
-                             int* launches);
+void launch_copy_anchors_out(const uint8_t* anchors, int prec, unsigned long long n, void* out, DevState* st,
+                             cudaStream_t s, int* launches);
 void launch_outliers_parse(const uint8_t* rec, int prec, unsigned long long count_max,
                            const unsigned long long* count_dev, unsigned long long n, uint64_t* oidx, double* oval,
                            DevState* st, cudaStream_t s, int* launches);

@@ -1,0 +1,20 @@
+// k_level_d.cu -- decompress instantiations of the tiled level kernels (k_level.cuh).
+#include "k_level.cuh"
+
+namespace hb {
+
+bool launch_level_tiled_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
+                                   const unsigned long long* ocount_dev, double* E, void* out, int prec, DevState* st,
+                                   cudaStream_t s) {
+  LvArgs A{};
+  A.E = E;
+  A.seq = const_cast<uint8_t*>(seq);
+  A.oidx = oidx;
+  A.oval = oval;
+  A.ocount = ocount_dev;
+  A.out = out;
+  A.st = st;
+  return launch_tiled<true>(g, A, prec, s);
+}
+
+}  // namespace hb

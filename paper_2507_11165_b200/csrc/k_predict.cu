@@ -88,6 +88,18 @@ void make_level_geom(const uint64_t dims[3], int level, LevelGeom* g) {
   long long pre = 1;
   for (int a = 0; a < 3; a++) pre *= (g->d[a] + (1ll << level) - 1) >> level;
   g->prefix = pre;
+  g->kl[0] = 2 * s * g->d[1] * g->d[2];
+  g->kl[1] = 2 * s * g->d[2];
+  g->kl[2] = 2 * s;
+  g->ke[0] = s * g->Ed[1] * g->Ed[2];
+  g->ke[1] = s * g->Ed[2];
+  g->ke[2] = s;
+  const long long ey = (g->D[1] + 1) >> 1, ez = (g->D[2] + 1) >> 1;
+  g->eyez = ey * ez;
+  g->ez = ez;
+  g->ks0 = 2 * g->D[1] * g->D[2] - ey * ez;
+  g->ks1_odd0 = 2 * g->D[2];
+  g->ks1_even0 = 2 * g->D[2] - ez;
 }
 
 // ---------------------------------------------------------- value range
@@ -250,22 +262,23 @@ void launch_anchor_load(const uint8_t* anchors, int prec, const uint64_t dims[3]
 
 // stride-1 archives (every point an anchor): anchors are the field
 template <typename T>
-__global__ void k_copy_anchors_out(const uint8_t* __restrict__ anc, unsigned long long n, T* out) {
+__global__ void k_copy_anchors_out(const uint8_t* __restrict__ anc, unsigned long long n, T* out, DevState* st) {
   unsigned long long j = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   T v;
   uint8_t* b = reinterpret_cast<uint8_t*>(&v);
   for (int k = 0; k < (int)sizeof(T); k++) b[k] = anc[j * sizeof(T) + k];
   out[j] = v;
+  if (!isfinite((double)v)) raise_flag(st, F_NONFINITE);
 }
 
-void launch_copy_anchors_out(const uint8_t* anchors, int prec, unsigned long long n, void* out, cudaStream_t s,
-                             int* launches) {
+void launch_copy_anchors_out(const uint8_t* anchors, int prec, unsigned long long n, void* out, DevState* st,
+                             cudaStream_t s, int* launches) {
   unsigned blocks = (unsigned)cdiv(n, 256);
   if (prec == 4)
-    k_copy_anchors_out<float><<<blocks, 256, 0, s>>>(anchors, n, (float*)out);
+    k_copy_anchors_out<float><<<blocks, 256, 0, s>>>(anchors, n, (float*)out, st);
   else
-    k_copy_anchors_out<double><<<blocks, 256, 0, s>>>(anchors, n, (double*)out);
+    k_copy_anchors_out<double><<<blocks, 256, 0, s>>>(anchors, n, (double*)out, st);
   (*launches)++;
 }
 
@@ -434,6 +447,7 @@ __device__ void run_tile(const LevelGeom& g, const TileCtx& t, double* sm, unsig
               E[((x0 >> 1) * e1 + (x1 >> 1)) * e2 + (x2 >> 1)] = r;
             else
               out[lin] = (T)r;
+            if (!isfinite(r)) raise_flag(st, F_NONFINITE);
           }
         }
         if (g.off[c] >= 0) sm[g.off[c] + (l[0] * ec[1] + l[1]) * ec[2] + l[2]] = r;
@@ -482,6 +496,7 @@ __global__ void __launch_bounds__(256) k_level(LevelGeom g, const T* __restrict_
           const bool owned = l0 >= t.eoff[0] && l0 < t.eoff[0] + t.ne[0] && l1 >= t.eoff[1] &&
                              l1 < t.eoff[1] + t.ne[1] && l2 >= t.eoff[2] && l2 < t.eoff[2] + t.ne[2];
           if (owned) out[((2 * h0) * g.d[1] + 2 * h1) * g.d[2] + 2 * h2] = (T)v;
+          if (owned && !isfinite(v)) raise_flag(st, F_NONFINITE);
         }
       }
       sm[idx] = v;
@@ -583,7 +598,10 @@ __global__ void __launch_bounds__(256) k_outlier_compact(const uint32_t* __restr
     // block scan over warps (lane 0 of each warp contributes)
     unsigned long long wexcl = block_excl_scan<unsigned long long>(lane == 0 ? wsum : 0ull, sh, &total);
     wexcl = __shfl_sync(0xffffffffu, wexcl, 0);
-    if (threadIdx.x == 0) base_sh = lookback(status, tile, total);
+    if (threadIdx.x < 32) {
+      const unsigned long long ex_ = lookback_warp(status, tile, total);
+      if (threadIdx.x == 0) base_sh = ex_;
+    }
     __syncthreads();
     unsigned long long r = base_sh + wexcl;
     if (total) {

@@ -191,7 +191,10 @@ __device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage, i
     unsigned long long total;
     unsigned long long wex = block_excl_scan<unsigned long long>(lane == 0 ? cnt : 0u, sh, &total);
     wex = __shfl_sync(0xffffffffu, wex, 0);
-    if (threadIdx.x == 0) base_sh = lookback(status, tile, total);
+    if (threadIdx.x < 32) {
+      const unsigned long long ex_ = lookback_warp(status, tile, total);
+      if (threadIdx.x == 0) base_sh = ex_;
+    }
     __syncthreads();
     unsigned long long r = base_sh + wex;
 #pragma unroll
@@ -519,17 +522,16 @@ __global__ void k_huff_zero(uint32_t* rec_words, DevState* st) {
 
 constexpr int HE_SYMS = 32;  // symbols per thread
 constexpr int HE_TILE = 256 * HE_SYMS;
+constexpr int HE_SMEM_WORDS = HE_TILE * 2 + 2;  // 64 bits per symbol worst case
 
-__device__ __forceinline__ void emit_word(uint32_t* words, unsigned long long wi, uint32_t be, bool owned) {
-  const uint32_t le = __byte_perm(be, 0, 0x0123);
-  if (owned)
-    words[wi] = le;
-  else
-    atomicOr(&words[wi], le);
-}
-
+// Each tile (8192 symbols) packs its codes MSB-first into a shared-memory bit
+// buffer (smem atomics only where two threads share a word), then streams the
+// whole-word range out with coalesced stores; only the first and last word of
+// a tile can be shared with a neighbouring tile and use a global atomicOr
+// (payload zeroed beforehand).
 __global__ void __launch_bounds__(256) k_huff_encode(const uint8_t* __restrict__ in, unsigned long long n,
                                                      uint32_t* rec_words, unsigned long long* lb, DevState* st) {
+  extern __shared__ uint32_t hbuf[];
   __shared__ uint8_t slen[256];
   __shared__ unsigned long long scode[256];
   __shared__ unsigned long long sh[33];
@@ -560,34 +562,69 @@ __global__ void __launch_bounds__(256) k_huff_encode(const uint8_t* __restrict__
     for (int k = 0; k < HE_SYMS; k++) nb += s0 + k < n ? slen[sym[k]] : 0;
     unsigned long long total;
     const unsigned long long excl = block_excl_scan<unsigned long long>(nb, sh, &total);
-    if (threadIdx.x == 0) base_sh = lookback(lb + 1, tile, total);
+    if (threadIdx.x < 32) {
+      const unsigned long long ex_ = lookback_warp(lb + 1, tile, total);
+      if (threadIdx.x == 0) base_sh = ex_;
+    }
     __syncthreads();
-    const unsigned long long start = 274ull * 8 + base_sh + excl, end = start + nb;
-    if (nb) {
-      unsigned long long wi = start >> 5;
+    const unsigned long long tstart = 274ull * 8 + base_sh;  // tile's first bit in the record
+    const int shift0 = (int)(tstart & 31);
+    const unsigned long long w0 = tstart >> 5;
+    const unsigned long long nwords = (shift0 + total + 31) >> 5;
+    if (nwords <= HE_SMEM_WORDS) {
+      for (unsigned i = threadIdx.x; i < nwords; i += blockDim.x) hbuf[i] = 0;
+      __syncthreads();
+      unsigned long long bit = shift0 + excl;  // local bit position
       uint64_t acc = 0;
-      int nacc = (int)(start & 31);  // leading bits of the first word belong to others
+      int nacc = (int)(bit & 31);
+      unsigned wi = (unsigned)(bit >> 5);
       for (int k = 0; k < HE_SYMS; k++) {
         if (s0 + k >= n) break;
         int L = slen[sym[k]];
         const unsigned long long c = scode[sym[k]];
         while (L > 0) {
-          const int take = L > 32 ? L - 32 : L;  // high part first for codes > 32 bits
-          const uint64_t part = (c >> (L - take)) & ((1ull << take) - 1);
-          acc = (acc << take) | part;
+          const int take = L > 32 ? L - 32 : L;
+          acc = (acc << take) | ((c >> (L - take)) & ((1ull << take) - 1));
           nacc += take;
           L -= take;
           if (nacc >= 32) {
-            const uint32_t be = (uint32_t)(acc >> (nacc - 32));
-            const bool owned = (wi << 5) >= start && ((wi + 1) << 5) <= end;
-            emit_word(rec_words, wi, be, owned);
-            wi++;
+            atomicOr(&hbuf[wi++], (uint32_t)(acc >> (nacc - 32)));
             nacc -= 32;
             acc &= nacc ? ((1ull << nacc) - 1) : 0ull;
           }
         }
       }
-      if (nacc > 0) emit_word(rec_words, wi, (uint32_t)(acc << (32 - nacc)), false);
+      if (nacc > 0) atomicOr(&hbuf[wi], (uint32_t)(acc << (32 - nacc)));
+      __syncthreads();
+      for (unsigned i = threadIdx.x; i < nwords; i += blockDim.x) {
+        const uint32_t le = __byte_perm(hbuf[i], 0, 0x0123);
+        if (i == 0 || i == nwords - 1)
+          atomicOr(&rec_words[w0 + i], le);
+        else
+          rec_words[w0 + i] = le;
+      }
+    } else if (nb) {  // oversized tile (codes > 64 bits on average): direct global atomics
+      const unsigned long long start = tstart + excl;
+      unsigned long long wi = start >> 5;
+      uint64_t acc = 0;
+      int nacc = (int)(start & 31);
+      for (int k = 0; k < HE_SYMS; k++) {
+        if (s0 + k >= n) break;
+        int L = slen[sym[k]];
+        const unsigned long long c = scode[sym[k]];
+        while (L > 0) {
+          const int take = L > 32 ? L - 32 : L;
+          acc = (acc << take) | ((c >> (L - take)) & ((1ull << take) - 1));
+          nacc += take;
+          L -= take;
+          if (nacc >= 32) {
+            atomicOr(&rec_words[wi++], __byte_perm((uint32_t)(acc >> (nacc - 32)), 0, 0x0123));
+            nacc -= 32;
+            acc &= nacc ? ((1ull << nacc) - 1) : 0ull;
+          }
+        }
+      }
+      if (nacc > 0) atomicOr(&rec_words[wi], __byte_perm((uint32_t)(acc << (32 - nacc)), 0, 0x0123));
     }
     __syncthreads();
   }
@@ -598,8 +635,14 @@ void launch_huffman_encode(const uint8_t* seq, unsigned long long n, uint8_t* hf
   k_huff_zero<<<PERSIST_CTAS, 256, 0, s>>>(reinterpret_cast<uint32_t*>(hf_rec), st);
   (*launches)++;
   if (n == 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_huff_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, HE_SMEM_WORDS * 4);
+    attr = true;
+  }
   const unsigned long long tiles = cdiv(n, HE_TILE);
-  k_huff_encode<<<persist_grid(tiles), 256, 0, s>>>(seq, n, reinterpret_cast<uint32_t*>(hf_rec), lb_ws, st);
+  k_huff_encode<<<persist_grid(tiles), 256, HE_SMEM_WORDS * 4, s>>>(seq, n, reinterpret_cast<uint32_t*>(hf_rec),
+                                                                   lb_ws, st);
   (*launches)++;
 }
 
@@ -748,7 +791,10 @@ __global__ void __launch_bounds__(RD_THREADS)
     unsigned long long total;
     unsigned long long wex = block_excl_scan<unsigned long long>(lane == 0 ? cnt : 0u, sh, &total);
     wex = __shfl_sync(0xffffffffu, wex, 0);
-    if (threadIdx.x == 0) base_sh = lookback(lb + 1, tile, total);
+    if (threadIdx.x < 32) {
+      const unsigned long long ex_ = lookback_warp(lb + 1, tile, total);
+      if (threadIdx.x == 0) base_sh = ex_;
+    }
     __syncthreads();
     unsigned long long r = base_sh + wex;  // ones before this warp's words
     if (stg == 2 && tile == 0 && threadIdx.x == 0 && !(mask[0] >> 31)) raise_flag(st, F_STAGE, 121);
@@ -941,7 +987,10 @@ void launch_bit_encode(const uint8_t* in, const unsigned long long* n_dev, int w
 // subsequence end, then passes re-decode only where a predecessor's end
 // disagrees with the guess (canonical prefix codes resynchronise within a
 // few codewords).  An exclusive scan of per-subsequence symbol counts gives
-// the output offsets for the final decode.
+// the output offsets for the final decode.  Decoding uses a 12-bit LUT in
+// shared memory plus a canonical slow path for longer codes; when the most
+// frequent symbol has the 1-bit code "0" (smooth fields) runs of zero bits
+// are consumed with one clz.  Output goes out in aligned 16-byte stores.
 
 constexpr int HD_S = 1024;       // bits per subsequence
 constexpr int HD_K = 12;         // LUT bits
@@ -950,6 +999,7 @@ constexpr int HD_PASSES = 4;
 struct HDTables {
   int ok;
   int maxlen, K;
+  int run_sym;  // symbol with the 1-bit code "0", or -1
   unsigned long long nsym, nbits, pay_off, pay_len, nsub;
   unsigned long long first_code[64];
   int first_rank[64], count[64];
@@ -965,79 +1015,125 @@ struct HDWork {  // per pass: start, end, count per subsequence
   int* changed;  // per pass
 };
 
-__global__ void k_hd_setup(const uint8_t* rec, const unsigned long long* len_dev, unsigned long long n_expect,
-                           unsigned long long max_out, HDTables* T, DevState* st) {
-  T->ok = 0;
-  if (st->flags & (F_STAGE | F_ARCHIVE)) return;
-  const unsigned long long n = *len_dev;
-  if (n < 10 || rec[0] != 1) return raise_flag(st, F_STAGE, 150);
-  const int w = rec[1];
-  if (w != 1 && w != 2 && w != 4 && w != 8) return raise_flag(st, F_STAGE, 151);
-  if (w != 1) return raise_flag(st, F_STAGE, 152);
-  if (n < 10 + 8 + 256) return raise_flag(st, F_STAGE, 153);
-  const unsigned long long nsym = ld_bytes(rec + 2, 8), nbits = ld_bytes(rec + 10, 8);
-  const uint8_t* len = rec + 18;
-  const unsigned long long plen = n - 274;
-  if (n_expect != ~0ull && nsym != n_expect) return raise_flag(st, F_ARCHIVE, 159);
-  if (nsym > max_out) return raise_flag(st, F_STAGE, 159);
-  T->nsym = nsym;
-  T->nbits = nbits;
-  T->pay_off = 274;
-  T->pay_len = plen;
-  st->hd_nsym = nsym;
-  if (nsym == 0) {
-    if (nbits || plen) return raise_flag(st, F_STAGE, 154);
-    T->ok = 1;
-    T->nsub = 0;
-    return;
+// stages.py:332-368: record checks, Kraft, canonical tables, LUT (parallel)
+__global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsigned long long* len_dev,
+                                                  unsigned long long n_expect, unsigned long long max_out,
+                                                  HDTables* T, DevState* st) {
+  __shared__ int ok_sh, cnt[257], maxlen_sh;
+  __shared__ uint8_t len[256];
+  const int t = threadIdx.x;
+  if (t == 0) {
+    T->ok = 0;
+    ok_sh = 0;
+    maxlen_sh = 0;
+    do {
+      if (st->flags & (F_STAGE | F_ARCHIVE)) break;
+      const unsigned long long n = *len_dev;
+      if (n < 10 || rec[0] != 1) { raise_flag(st, F_STAGE, 150); break; }
+      const int w = rec[1];
+      if (w != 1 && w != 2 && w != 4 && w != 8) { raise_flag(st, F_STAGE, 151); break; }
+      if (w != 1) { raise_flag(st, F_STAGE, 152); break; }
+      if (n < 10 + 8 + 256) { raise_flag(st, F_STAGE, 153); break; }
+      const unsigned long long nsym = ld_bytes(rec + 2, 8), nbits = ld_bytes(rec + 10, 8);
+      const unsigned long long plen = n - 274;
+      if (n_expect != ~0ull && nsym != n_expect) { raise_flag(st, F_ARCHIVE, 159); break; }
+      if (nsym > max_out) { raise_flag(st, F_STAGE, 159); break; }
+      T->nsym = nsym;
+      T->nbits = nbits;
+      T->pay_off = 274;
+      T->pay_len = plen;
+      st->hd_nsym = nsym;
+      if (nsym == 0) {
+        if (nbits || plen) { raise_flag(st, F_STAGE, 154); break; }
+        T->nsub = 0;
+        T->ok = 1;
+        break;
+      }
+      if (nbits / 8 + (nbits % 8 != 0) != plen) { raise_flag(st, F_STAGE, 155); break; }
+      if (nbits == 0) { raise_flag(st, F_STAGE, 155); break; }
+      ok_sh = 1;
+    } while (0);
   }
-  if (nbits / 8 + (nbits % 8 != 0) != plen) return raise_flag(st, F_STAGE, 155);
-  if (nbits == 0) return raise_flag(st, F_STAGE, 155);
-  int cnt[256];
-  for (int L = 0; L < 256; L++) cnt[L] = 0;
-  int ns = 0, maxlen = 0;
-  for (int s = 0; s < 256; s++)
-    if (len[s]) {
-      cnt[len[s]]++;
-      ns++;
-      maxlen = len[s] > maxlen ? len[s] : maxlen;
+  __syncthreads();
+  if (!ok_sh) return;
+  len[t] = rec[18 + t];
+  cnt[t] = 0;
+  if (t == 0) cnt[256] = 0;
+  __syncthreads();
+  if (len[t]) {
+    atomicAdd(&cnt[len[t]], 1);
+    atomicMax(&maxlen_sh, (int)len[t]);
+  }
+  __syncthreads();
+  const int maxlen = maxlen_sh;
+  if (t == 0) {
+    int ns = 0;
+    for (int L = 1; L <= 255; L++) ns += cnt[L];
+    bool good = ns > 0;
+    if (!good) raise_flag(st, F_STAGE, 156);
+    long long avail = 1;
+    for (int L = 1; L <= maxlen && good; L++) {  // Kraft, exact with a cap
+      avail = avail * 2 - cnt[L];
+      if (avail < 0) {
+        raise_flag(st, F_STAGE, 157);
+        good = false;
+      }
+      if (avail > 1024) avail = 1024;
     }
-  if (ns == 0) return raise_flag(st, F_STAGE, 156);
-  long long avail = 1;
-  for (int L = 1; L <= maxlen; L++) {
-    avail = avail * 2 - cnt[L];
-    if (avail < 0) return raise_flag(st, F_STAGE, 157);
-    if (avail > 1024) avail = 1024;
-  }
-  if (maxlen > 56) return raise_flag(st, F_UNSUPPORTED, 158);
-  // canonical tables
-  int r = 0;
-  unsigned long long next = 0;
-  int prev = 0;
-  for (int L = 0; L < 64; L++) T->first_rank[L] = -1, T->count[L] = 0, T->first_code[L] = 0;
-  for (int L = 1; L <= maxlen; L++)
-    for (int s = 0; s < 256; s++)
-      if (len[s] == L) {
+    if (good && maxlen > 56) {
+      raise_flag(st, F_UNSUPPORTED, 158);
+      good = false;
+    }
+    if (good) {
+      unsigned long long next = 0;
+      int prev = 0, r = 0;
+      for (int L = 0; L < 64; L++) T->first_rank[L] = -1, T->count[L] = 0, T->first_code[L] = 0;
+      for (int L = 1; L <= maxlen; L++) {
+        if (!cnt[L]) continue;
         next <<= (L - prev);
         prev = L;
-        if (T->first_rank[L] < 0) T->first_rank[L] = r, T->first_code[L] = next;
-        T->count[L]++;
-        T->syms[r++] = (uint8_t)s;
-        next++;
+        T->first_rank[L] = r;
+        T->first_code[L] = next;
+        T->count[L] = cnt[L];
+        next += cnt[L];
+        r += cnt[L];
       }
-  const int K = maxlen < HD_K ? maxlen : HD_K;
-  T->maxlen = maxlen;
-  T->K = K;
-  for (int i = 0; i < (1 << HD_K); i++) T->lut[i] = 0;
-  for (int L = 1; L <= K; L++)
-    for (int q = 0; q < T->count[L]; q++) {
-      const unsigned long long code = T->first_code[L] + q;
-      const int sym = T->syms[T->first_rank[L] + q];
-      const unsigned long long lo = code << (K - L), cntk = 1ull << (K - L);
-      for (unsigned long long x = 0; x < cntk; x++) T->lut[lo + x] = (uint16_t)((L << 8) | sym);
+      T->maxlen = maxlen;
+      T->K = maxlen < HD_K ? maxlen : HD_K;
+      T->nsub = cdiv(T->nbits, HD_S);
     }
-  T->nsub = cdiv(nbits, HD_S);
-  T->ok = 1;
+    ok_sh = good;
+  }
+  __syncthreads();
+  if (!ok_sh) return;
+  // sorted symbol list: rank of symbol t among (len, sym)
+  if (len[t]) {
+    int r = 0;
+    for (int L = 1; L < len[t]; L++) r += cnt[L];
+    for (int j = 0; j < t; j++) r += len[j] == len[t];
+    T->syms[r] = (uint8_t)t;
+  }
+  __syncthreads();
+  const int K = T->K;
+  for (int e = t; e < (1 << HD_K); e += 256) {
+    uint16_t v = 0;
+    if (e < (1 << K)) {
+      for (int L = 1; L <= K; L++) {
+        if (!T->count[L]) continue;
+        const unsigned long long c = (unsigned long long)e >> (K - L);
+        if (c >= T->first_code[L] && c - T->first_code[L] < (unsigned long long)T->count[L]) {
+          v = (uint16_t)((L << 8) | T->syms[T->first_rank[L] + (int)(c - T->first_code[L])]);
+          break;
+        }
+      }
+    }
+    T->lut[e] = v;
+  }
+  if (t == 0) {
+    T->run_sym = (T->count[1] > 0 && T->first_code[1] == 0) ? T->syms[T->first_rank[1]] : -1;
+    __threadfence();
+    T->ok = 1;
+  }
 }
 
 struct BitReader {
@@ -1066,22 +1162,91 @@ struct BitReader {
     }
   }
   __device__ __forceinline__ void consume(int L) {
-    buf <<= L;
+    buf = L >= 64 ? 0 : buf << L;
     nb -= L;
     if (nb <= 56) refill();
   }
 };
 
+// 16-byte aligned output writer for one thread's contiguous output range
+struct OutWriter {
+  uint8_t* out;
+  unsigned long long start, p;
+  uint64_t lo, hi;
+  unsigned zeros;
+  __device__ void init(uint8_t* o, unsigned long long s) {
+    out = o;
+    start = p = s;
+    lo = hi = 0;
+    zeros = 0;
+  }
+  __device__ __forceinline__ void flush_chunk(unsigned long long base, int upto) {  // bytes [base, base+upto)
+    if (base >= start && upto == 16) {
+      *reinterpret_cast<uint4*>(out + base) = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi,
+                                                        (uint32_t)(hi >> 32));
+    } else {
+      for (int k = 0; k < upto; k++) {
+        if (base + k < start) continue;
+        out[base + k] = (uint8_t)(k < 8 ? (lo >> (8 * k)) : (hi >> (8 * (k - 8))));
+      }
+    }
+    lo = hi = 0;
+  }
+  __device__ __forceinline__ void put(int b) {
+    const int k = (int)(p & 15);
+    if (k < 8)
+      lo |= (uint64_t)b << (8 * k);
+    else
+      hi |= (uint64_t)b << (8 * (k - 8));
+    p++;
+    if (!(p & 15)) flush_chunk(p - 16, 16);
+  }
+  __device__ __forceinline__ void run(int b, unsigned long long n) {
+    while (n && (p & 15)) {
+      put(b);
+      n--;
+    }
+    const uint64_t rep = 0x0101010101010101ull * (uint64_t)b;
+    while (n >= 16) {
+      lo = hi = rep;
+      flush_chunk(p, 16);
+      p += 16;
+      n -= 16;
+    }
+    while (n) {
+      put(b);
+      n--;
+    }
+  }
+  __device__ void finish() {
+    if (p & 15) flush_chunk(p & ~15ull, (int)(p & 15));
+  }
+};
+
 // decode from `start` while pos < stop (and < nbits); returns symbols or -1 on error
+template <bool EMIT>
 __device__ long long hd_decode(const HDTables& T, const uint16_t* lut, const uint8_t* pay, unsigned long long start,
-                               unsigned long long stop, unsigned long long* endp, uint8_t* out, unsigned* zeros) {
+                               unsigned long long stop, unsigned long long* endp, OutWriter* ow) {
   BitReader br;
   br.init(pay, T.pay_len, start);
   unsigned long long pos = start;
   long long cnt = 0;
-  const unsigned long long nbits = T.nbits;
-  const int K = T.K;
-  while (pos < stop && pos < nbits) {
+  const unsigned long long lim = stop < T.nbits ? stop : T.nbits;
+  const int K = T.K, rs = T.run_sym;
+  while (pos < lim) {
+    if (rs >= 0 && !(br.buf >> 63)) {  // run of the 1-bit code "0"
+      unsigned long long z = br.buf ? (unsigned long long)__clzll(br.buf) : 64ull;
+      if (z > (unsigned long long)br.nb) z = br.nb;
+      if (z > lim - pos) z = lim - pos;
+      if (EMIT) {
+        ow->run(rs, z);
+        if (rs == 0) ow->zeros += (unsigned)z;
+      }
+      pos += z;
+      cnt += (long long)z;
+      br.consume((int)z);
+      continue;
+    }
     const uint16_t e = lut[br.buf >> (64 - K)];
     int L, sym;
     if (e) {
@@ -1102,13 +1267,13 @@ __device__ long long hd_decode(const HDTables& T, const uint16_t* lut, const uin
         return -1;
       }
     }
-    if (pos + L > nbits) {
+    if (pos + L > T.nbits) {
       *endp = pos;
       return -1;
     }
-    if (out) {
-      out[cnt] = (uint8_t)sym;
-      if (zeros) *zeros += sym == 0;
+    if (EMIT) {
+      ow->put(sym);
+      ow->zeros += sym == 0;
     }
     pos += L;
     cnt++;
@@ -1121,7 +1286,7 @@ __device__ long long hd_decode(const HDTables& T, const uint16_t* lut, const uin
 __global__ void __launch_bounds__(256) k_hd_first(const uint8_t* rec, const HDTables* T, HDWork W, DevState* st) {
   __shared__ uint16_t lut[1 << HD_K];
   if (!T->ok) return;
-  for (int i = threadIdx.x; i < (1 << HD_K); i++) lut[i] = T->lut[i];
+  for (int i = threadIdx.x; i < (1 << HD_K); i += blockDim.x) lut[i] = T->lut[i];
   __syncthreads();
   const unsigned long long nsub = T->nsub;
   const uint8_t* pay = rec + T->pay_off;
@@ -1129,7 +1294,7 @@ __global__ void __launch_bounds__(256) k_hd_first(const uint8_t* rec, const HDTa
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned long long s0 = i * HD_S;
     unsigned long long e;
-    const long long c = hd_decode(*T, lut, pay, s0, s0 + HD_S, &e, nullptr, nullptr);
+    const long long c = hd_decode<false>(*T, lut, pay, s0, s0 + HD_S, &e, nullptr);
     W.s[0][i] = s0;
     W.e[0][i] = c < 0 ? ~0ull : e;  // error end never matches a successor start
     W.c[0][i] = c < 0 ? 0u : (unsigned)c;
@@ -1151,7 +1316,7 @@ __global__ void __launch_bounds__(256) k_hd_pass(int p, const uint8_t* rec, cons
     }
     return;
   }
-  for (int i = threadIdx.x; i < (1 << HD_K); i++) lut[i] = T->lut[i];
+  for (int i = threadIdx.x; i < (1 << HD_K); i += blockDim.x) lut[i] = T->lut[i];
   __syncthreads();
   const uint8_t* pay = rec + T->pay_off;
   bool ch = false;
@@ -1163,9 +1328,9 @@ __global__ void __launch_bounds__(256) k_hd_pass(int p, const uint8_t* rec, cons
       W.e[wr][i] = W.e[rd][i];
       W.c[wr][i] = W.c[rd][i];
     } else {
-      unsigned long long e;
-      const long long c = want >= (i + 1) * HD_S ? 0 : hd_decode(*T, lut, pay, want, (i + 1) * HD_S, &e, nullptr, nullptr);
-      if (want >= (i + 1) * HD_S) e = want;
+      unsigned long long e = want;
+      long long c = 0;
+      if (want < (i + 1) * HD_S) c = hd_decode<false>(*T, lut, pay, want, (i + 1) * HD_S, &e, nullptr);
       W.s[wr][i] = want;
       W.e[wr][i] = c < 0 ? ~0ull : e;
       W.c[wr][i] = c < 0 ? 0u : (unsigned)c;
@@ -1198,7 +1363,10 @@ __global__ void __launch_bounds__(256) k_hd_scan(const HDTables* T, HDWork W, in
     }
     unsigned long long total;
     const unsigned long long ex = block_excl_scan<unsigned long long>(sum, sh, &total);
-    if (threadIdx.x == 0) base_sh = lookback(lb + 1, tile, total);
+    if (threadIdx.x < 32) {
+      const unsigned long long ex_ = lookback_warp(lb + 1, tile, total);
+      if (threadIdx.x == 0) base_sh = ex_;
+    }
     __syncthreads();
     unsigned long long r = base_sh + ex;
 #pragma unroll
@@ -1221,7 +1389,7 @@ __global__ void __launch_bounds__(256) k_hd_emit(const uint8_t* rec, const HDTab
   __shared__ uint16_t lut[1 << HD_K];
   if (!T->ok) return;
   if (st->flags & F_STAGE) return;
-  for (int i = threadIdx.x; i < (1 << HD_K); i++) lut[i] = T->lut[i];
+  for (int i = threadIdx.x; i < (1 << HD_K); i += blockDim.x) lut[i] = T->lut[i];
   __syncthreads();
   const unsigned long long nsub = T->nsub;
   const uint8_t* pay = rec + T->pay_off;
@@ -1235,11 +1403,16 @@ __global__ void __launch_bounds__(256) k_hd_emit(const uint8_t* rec, const HDTab
       bad = true;
       continue;
     }
+    OutWriter ow;
+    ow.init(out, W.off[i]);
     unsigned long long e;
-    const long long c = hd_decode(*T, lut, pay, s0, (i + 1) * HD_S, &e, out + W.off[i], &zeros);
+    const long long c = hd_decode<true>(*T, lut, pay, s0, (i + 1) * HD_S, &e, &ow);
+    ow.finish();
+    zeros += ow.zeros;
     bad |= c < 0;
   }
-  if (zeros) atomicAdd(&st->zero_count, (unsigned long long)zeros);
+  zeros = warp_sum<unsigned>(zeros);
+  if ((threadIdx.x & 31) == 0 && zeros) atomicAdd(&st->zero_count, (unsigned long long)zeros);
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) raise_flag(st, F_STAGE, 162);
 }
 
@@ -1255,9 +1428,9 @@ __global__ void k_hd_serial(const uint8_t* rec, const HDTables* T, HDWork W, int
       continue;
     }
     if (want == W.s[fin][i]) continue;
-    unsigned long long e;
-    long long c = want >= (i + 1) * HD_S ? 0 : hd_decode(*T, T->lut, pay, want, (i + 1) * HD_S, &e, nullptr, nullptr);
-    if (want >= (i + 1) * HD_S) e = want;
+    unsigned long long e = want;
+    long long c = 0;
+    if (want < (i + 1) * HD_S) c = hd_decode<false>(*T, T->lut, pay, want, (i + 1) * HD_S, &e, nullptr);
     W.s[fin][i] = want;
     W.e[fin][i] = c < 0 ? ~0ull : e;
     W.c[fin][i] = c < 0 ? 0u : (unsigned)c;
@@ -1290,7 +1463,7 @@ void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long*
     p += nsub_max * 4;
   }
   W.changed = reinterpret_cast<int*>(p);  // HD_PASSES + 1 ints, zeroed by the caller
-  k_hd_setup<<<1, 1, 0, s>>>(hf_rec, len_dev, n, max_out, T, st);
+  k_hd_setup<<<1, 256, 0, s>>>(hf_rec, len_dev, n, max_out, T, st);
   (*launches)++;
   const unsigned g = persist_grid(cdiv(nsub_max, 256));
   k_hd_first<<<g, 256, 0, s>>>(hf_rec, T, W, st);
