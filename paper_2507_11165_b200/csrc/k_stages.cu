@@ -161,29 +161,27 @@ __device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage, i
     const unsigned long long tile = tile_sh;
     if (tile >= ntiles) break;
     const unsigned long long w0 = tile * RD_TILE + (unsigned long long)wid * 1024;
-    uint64_t word[32];
-    uint32_t mask[32];
+    uint32_t my_mask = 0;  // lane k keeps the keep-mask of step k
     unsigned cnt = 0;
     uint64_t prev_last = 0;
-#pragma unroll
     for (int k = 0; k < 32; k++) {
       const unsigned long long i = w0 + k * 32 + lane;
+      if (w0 + k * 32 >= nw) break;  // warp-uniform
       const bool in = i < nw;
       const uint64_t v = in ? src.word(i) : 0;
-      word[k] = v;
       bool keep;
       if (stage == 2) {
         uint64_t pv = __shfl_up_sync(0xffffffffu, v, 1);
-        if (lane == 0) pv = k == 0 ? (i > 0 && i - 1 < nw ? src.word(i - 1) : ~v) : prev_last;
+        if (lane == 0) pv = k == 0 ? (i > 0 ? src.word(i - 1) : ~v) : prev_last;
         keep = in && (i == 0 || v != pv);
       } else {
         keep = in && v != 0;
       }
       prev_last = __shfl_sync(0xffffffffu, v, 31);
       const uint32_t m = __ballot_sync(0xffffffffu, keep);
-      mask[k] = m;
+      if (lane == k) my_mask = m;
       cnt += __popc(m);
-      if (lane == 0 && w0 + k * 32 < nw) {
+      if (lane == 0) {
         const uint32_t be = __brev(m);  // word 0 at the MSB (np.packbits order)
         *reinterpret_cast<uint32_t*>(bitmap + (w0 + k * 32) / 8) = __byte_perm(be, 0, 0x0123);
       }
@@ -197,20 +195,22 @@ __device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage, i
     }
     __syncthreads();
     unsigned long long r = base_sh + wex;
-#pragma unroll
     for (int k = 0; k < 32; k++) {
-      const uint32_t m = mask[k];
+      if (w0 + k * 32 >= nw) break;
+      const uint32_t m = __shfl_sync(0xffffffffu, my_mask, k);
       if ((m >> lane) & 1) {
+        const unsigned long long i = w0 + k * 32 + lane;
+        const uint64_t v = src.word(i);
         const unsigned long long dst = r + __popc(m & ((1u << lane) - 1));
         uint8_t* p = payload + dst * width;
         if (width == 1)
-          *p = (uint8_t)word[k];
+          *p = (uint8_t)v;
         else if (width == 2)
-          *reinterpret_cast<uint16_t*>(p) = (uint16_t)word[k];
+          *reinterpret_cast<uint16_t*>(p) = (uint16_t)v;
         else if (width == 4)
-          *reinterpret_cast<uint32_t*>(p) = (uint32_t)word[k];
+          *reinterpret_cast<uint32_t*>(p) = (uint32_t)v;
         else
-          *reinterpret_cast<uint64_t*>(p) = word[k];
+          *reinterpret_cast<uint64_t*>(p) = v;
       }
       r += __popc(m);
     }
@@ -532,12 +532,13 @@ constexpr int HE_SMEM_WORDS = HE_TILE * 2 + 2;  // 64 bits per symbol worst case
 __global__ void __launch_bounds__(256) k_huff_encode(const uint8_t* __restrict__ in, unsigned long long n,
                                                      uint32_t* rec_words, unsigned long long* lb, DevState* st) {
   extern __shared__ uint32_t hbuf[];
-  __shared__ uint8_t slen[256];
-  __shared__ unsigned long long scode[256];
+  __shared__ unsigned long long stab[256];  // code | len << 56
   __shared__ unsigned long long sh[33];
   __shared__ unsigned long long tile_sh, base_sh;
-  slen[threadIdx.x] = st->hf_len[threadIdx.x];
-  scode[threadIdx.x] = st->hf_code[threadIdx.x];
+  {
+    const unsigned long long L = st->hf_len[threadIdx.x];
+    stab[threadIdx.x] = st->hf_code[threadIdx.x] | (L << 56);
+  }
   __syncthreads();
   const unsigned long long ntiles = cdiv(n, HE_TILE);
   for (;;) {
@@ -546,20 +547,24 @@ __global__ void __launch_bounds__(256) k_huff_encode(const uint8_t* __restrict__
     const unsigned long long tile = tile_sh;
     if (tile >= ntiles) break;
     const unsigned long long s0 = tile * HE_TILE + (unsigned long long)threadIdx.x * HE_SYMS;
-    uint8_t sym[HE_SYMS];
-    if (s0 + HE_SYMS <= n) {
+    const int cnt = s0 >= n ? 0 : (s0 + HE_SYMS <= n ? HE_SYMS : (int)(n - s0));
+    uint32_t w[8];
+    if (cnt == HE_SYMS) {
       const uint4* p = reinterpret_cast<const uint4*>(in + s0);
       const uint4 a = p[0], b = p[1];
-      const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-      for (int k = 0; k < HE_SYMS; k++) sym[k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+      w[0] = a.x, w[1] = a.y, w[2] = a.z, w[3] = a.w, w[4] = b.x, w[5] = b.y, w[6] = b.z, w[7] = b.w;
     } else {
 #pragma unroll
-      for (int k = 0; k < HE_SYMS; k++) sym[k] = s0 + k < n ? in[s0 + k] : 0;
+      for (int q = 0; q < 8; q++) {
+        w[q] = 0;
+        for (int k = 0; k < 4; k++)
+          if (q * 4 + k < cnt) w[q] |= (uint32_t)in[s0 + q * 4 + k] << (8 * k);
+      }
     }
     unsigned nb = 0;
 #pragma unroll
-    for (int k = 0; k < HE_SYMS; k++) nb += s0 + k < n ? slen[sym[k]] : 0;
+    for (int k = 0; k < HE_SYMS; k++)
+      if (k < cnt) nb += (unsigned)(stab[(w[k >> 2] >> (8 * (k & 3))) & 0xFF] >> 56);
     unsigned long long total;
     const unsigned long long excl = block_excl_scan<unsigned long long>(nb, sh, &total);
     if (threadIdx.x < 32) {
@@ -571,31 +576,44 @@ __global__ void __launch_bounds__(256) k_huff_encode(const uint8_t* __restrict__
     const int shift0 = (int)(tstart & 31);
     const unsigned long long w0 = tstart >> 5;
     const unsigned long long nwords = (shift0 + total + 31) >> 5;
-    if (nwords <= HE_SMEM_WORDS) {
+    const bool in_smem = nwords <= HE_SMEM_WORDS;
+    if (in_smem)
       for (unsigned i = threadIdx.x; i < nwords; i += blockDim.x) hbuf[i] = 0;
-      __syncthreads();
-      unsigned long long bit = shift0 + excl;  // local bit position
-      uint64_t acc = 0;
-      int nacc = (int)(bit & 31);
-      unsigned wi = (unsigned)(bit >> 5);
-      for (int k = 0; k < HE_SYMS; k++) {
-        if (s0 + k >= n) break;
-        int L = slen[sym[k]];
-        const unsigned long long c = scode[sym[k]];
-        while (L > 0) {
-          const int take = L > 32 ? L - 32 : L;
-          acc = (acc << take) | ((c >> (L - take)) & ((1ull << take) - 1));
-          nacc += take;
-          L -= take;
-          if (nacc >= 32) {
-            atomicOr(&hbuf[wi++], (uint32_t)(acc >> (nacc - 32)));
-            nacc -= 32;
-            acc &= nacc ? ((1ull << nacc) - 1) : 0ull;
-          }
+    __syncthreads();
+    // OR only the non-zero bits: the all-zero canonical code (the most
+    // frequent symbol) just advances the bit position
+    unsigned long long pos = in_smem ? shift0 + excl : tstart + excl;
+#pragma unroll
+    for (int k = 0; k < HE_SYMS; k++) {
+      const unsigned long long e = k < cnt ? stab[(w[k >> 2] >> (8 * (k & 3))) & 0xFF] : 0ull;
+      const int L = (int)(e >> 56);
+      const unsigned long long c = e & ((1ull << 56) - 1);
+      if (c) {
+        // bits of c end at pos + L; split over at most 3 words
+        const unsigned long long end = pos + L;
+        unsigned long long wi = (end - 1) >> 5;
+        const int r = (int)(end & 31);  // bits of the last word used
+        unsigned long long v = c;
+        int left = L;
+        int first = r ? r : 32;
+        while (left > 0) {
+          const int take = left < first ? left : first;
+          const uint32_t chunk = (uint32_t)(v & ((1ull << take) - 1));
+          const uint32_t be = chunk << (32 - first);  // place within the word (MSB-first)
+          if (in_smem)
+            atomicOr(&hbuf[wi], be);
+          else
+            atomicOr(&rec_words[wi], __byte_perm(be, 0, 0x0123));
+          v >>= take;
+          left -= take;
+          wi--;
+          first = 32;
         }
       }
-      if (nacc > 0) atomicOr(&hbuf[wi], (uint32_t)(acc << (32 - nacc)));
-      __syncthreads();
+      pos += L;
+    }
+    __syncthreads();
+    if (in_smem) {
       for (unsigned i = threadIdx.x; i < nwords; i += blockDim.x) {
         const uint32_t le = __byte_perm(hbuf[i], 0, 0x0123);
         if (i == 0 || i == nwords - 1)
@@ -603,28 +621,6 @@ __global__ void __launch_bounds__(256) k_huff_encode(const uint8_t* __restrict__
         else
           rec_words[w0 + i] = le;
       }
-    } else if (nb) {  // oversized tile (codes > 64 bits on average): direct global atomics
-      const unsigned long long start = tstart + excl;
-      unsigned long long wi = start >> 5;
-      uint64_t acc = 0;
-      int nacc = (int)(start & 31);
-      for (int k = 0; k < HE_SYMS; k++) {
-        if (s0 + k >= n) break;
-        int L = slen[sym[k]];
-        const unsigned long long c = scode[sym[k]];
-        while (L > 0) {
-          const int take = L > 32 ? L - 32 : L;
-          acc = (acc << take) | ((c >> (L - take)) & ((1ull << take) - 1));
-          nacc += take;
-          L -= take;
-          if (nacc >= 32) {
-            atomicOr(&rec_words[wi++], __byte_perm((uint32_t)(acc >> (nacc - 32)), 0, 0x0123));
-            nacc -= 32;
-            acc &= nacc ? ((1ull << nacc) - 1) : 0ull;
-          }
-        }
-      }
-      if (nacc > 0) atomicOr(&rec_words[wi], __byte_perm((uint32_t)(acc << (32 - nacc)), 0, 0x0123));
     }
     __syncthreads();
   }
@@ -770,24 +766,20 @@ __global__ void __launch_bounds__(RD_THREADS)
     const unsigned long long tile = tile_sh;
     if (tile >= ntiles) break;
     const unsigned long long w0 = tile * RD_TILE + (unsigned long long)wid * 1024;
-    uint32_t mask[32];
-    unsigned cnt = 0;
-#pragma unroll
-    for (int j = 0; j < 32; j++) {
-      const unsigned long long i0 = w0 + j * 32;  // 32 words = 4 bitmap bytes
-      uint32_t m = 0;
+    // lane j fetches the bitmap word (32 symbols) of step j
+    uint32_t my_mask = 0;
+    {
+      const unsigned long long i0 = w0 + lane * 32;
       if (i0 < nsym) {
-        const unsigned long long bb = i0 >> 3;
+        const unsigned long long bb = i0 >> 3, nbm = cdiv(nsym, 8);
         uint32_t be = 0;
-        for (int q = 0; q < 4; q++) be |= (bb + q < cdiv(nsym, 8) ? (uint32_t)bm[bb + q] : 0u) << (24 - 8 * q);
+        for (int q = 0; q < 4; q++) be |= (bb + q < nbm ? (uint32_t)bm[bb + q] : 0u) << (24 - 8 * q);
         const unsigned long long valid = nsym - i0;
         if (valid < 32) be &= ~(0xFFFFFFFFu >> valid);
-        m = be;  // bit (31 - l) = word i0 + l
+        my_mask = be;  // bit (31 - l) = word i0 + l
       }
-      mask[j] = m;
-      cnt += __popc(m);
     }
-    // mask[] is warp-uniform; one lane's count is the warp's
+    const unsigned cnt = warp_sum<unsigned>(__popc(my_mask));
     unsigned long long total;
     unsigned long long wex = block_excl_scan<unsigned long long>(lane == 0 ? cnt : 0u, sh, &total);
     wex = __shfl_sync(0xffffffffu, wex, 0);
@@ -797,20 +789,20 @@ __global__ void __launch_bounds__(RD_THREADS)
     }
     __syncthreads();
     unsigned long long r = base_sh + wex;  // ones before this warp's words
-    if (stg == 2 && tile == 0 && threadIdx.x == 0 && !(mask[0] >> 31)) raise_flag(st, F_STAGE, 121);
-#pragma unroll
+    if (stg == 2 && tile == 0 && threadIdx.x == 0 && !(my_mask >> 31)) raise_flag(st, F_STAGE, 121);
     for (int j = 0; j < 32; j++) {
+      if (w0 + j * 32 >= nsym) break;  // warp-uniform
       const unsigned long long i = w0 + j * 32 + lane;
-      const uint32_t m = mask[j];
+      const uint32_t m = __shfl_sync(0xffffffffu, my_mask, j);
       if (i < nsym) {
         const int bit = (m >> (31 - lane)) & 1;
         const unsigned long long before = r + (lane ? __popc(m >> (32 - lane)) : 0);
         uint64_t v = 0;
         if (stg == 2) {
           const unsigned long long idx = before + bit;  // inclusive count
-          if (idx >= 1 && idx <= npay) v = ld_bytes(pay + (idx - 1) * w, w);
+          if (idx >= 1 && idx <= npay) v = w == 1 ? pay[idx - 1] : ld_bytes(pay + (idx - 1) * w, w);
         } else if (bit && before < npay) {
-          v = ld_bytes(pay + before * w, w);
+          v = w == 1 ? pay[before] : ld_bytes(pay + before * w, w);
         }
         uint8_t* p = out + i * w;
         if (w == 1)
@@ -1012,7 +1004,8 @@ struct HDWork {  // per pass: start, end, count per subsequence
   unsigned long long* e[2];
   unsigned* c[2];
   unsigned long long* off;
-  int* changed;  // per pass
+  unsigned long long* bmask;  // codeword starts in [i*S, i*S+64) seen by the first pass
+  int* changed;               // per pass
 };
 
 // stages.py:332-368: record checks, Kraft, canonical tables, LUT (parallel)
@@ -1223,21 +1216,43 @@ struct OutWriter {
   }
 };
 
-// decode from `start` while pos < stop (and < nbits); returns symbols or -1 on error
-template <bool EMIT>
+// decode from `start` while pos < stop (and < nbits); returns symbols or -1 on error.
+// MASK: record codeword starts in [start, start+64) into *mask.
+// SYNC: stop early at the first codeword start p with (p - sbase) < 64 and
+//       bit (p - sbase) of sync_mask set (*endp = p).
+template <bool EMIT, bool MASK = false, bool SYNC = false>
 __device__ long long hd_decode(const HDTables& T, const uint16_t* lut, const uint8_t* pay, unsigned long long start,
-                               unsigned long long stop, unsigned long long* endp, OutWriter* ow) {
+                               unsigned long long stop, unsigned long long* endp, OutWriter* ow,
+                               unsigned long long* mask = nullptr, unsigned long long sbase = 0,
+                               unsigned long long sync_mask = 0) {
   BitReader br;
   br.init(pay, T.pay_len, start);
   unsigned long long pos = start;
   long long cnt = 0;
+  unsigned long long m = 0;
   const unsigned long long lim = stop < T.nbits ? stop : T.nbits;
   const int K = T.K, rs = T.run_sym;
   while (pos < lim) {
+    if (SYNC) {
+      const unsigned long long q = pos - sbase;
+      if (q >= 64) break;  // no sync inside the window
+      if ((sync_mask >> q) & 1) {
+        *endp = pos;
+        return cnt;
+      }
+    }
+    if (MASK && pos - start < 64) m |= 1ull << (pos - start);
     if (rs >= 0 && !(br.buf >> 63)) {  // run of the 1-bit code "0"
       unsigned long long z = br.buf ? (unsigned long long)__clzll(br.buf) : 64ull;
       if (z > (unsigned long long)br.nb) z = br.nb;
       if (z > lim - pos) z = lim - pos;
+      if (SYNC) {  // advance one codeword at a time inside the sync window
+        z = 1;
+      }
+      if (MASK) {
+        const unsigned long long q = pos - start;
+        if (q < 64) m |= (z >= 64 ? ~0ull : ((1ull << z) - 1)) << q;
+      }
       if (EMIT) {
         ow->run(rs, z);
         if (rs == 0) ow->zeros += (unsigned)z;
@@ -1264,11 +1279,13 @@ __device__ long long hd_decode(const HDTables& T, const uint16_t* lut, const uin
       }
       if (sym < 0) {
         *endp = pos;
+        if (MASK) *mask = m;
         return -1;
       }
     }
     if (pos + L > T.nbits) {
       *endp = pos;
+      if (MASK) *mask = m;
       return -1;
     }
     if (EMIT) {
@@ -1280,6 +1297,8 @@ __device__ long long hd_decode(const HDTables& T, const uint16_t* lut, const uin
     br.consume(L);
   }
   *endp = pos;
+  if (MASK) *mask = m;
+  if (SYNC) return -2;  // window exhausted without sync (or hit the end): caller re-decodes fully
   return cnt;
 }
 
@@ -1293,8 +1312,9 @@ __global__ void __launch_bounds__(256) k_hd_first(const uint8_t* rec, const HDTa
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nsub;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned long long s0 = i * HD_S;
-    unsigned long long e;
-    const long long c = hd_decode<false>(*T, lut, pay, s0, s0 + HD_S, &e, nullptr);
+    unsigned long long e, m = 0;
+    const long long c = hd_decode<false, true>(*T, lut, pay, s0, s0 + HD_S, &e, nullptr, &m);
+    W.bmask[i] = m;
     W.s[0][i] = s0;
     W.e[0][i] = c < 0 ? ~0ull : e;  // error end never matches a successor start
     W.c[0][i] = c < 0 ? 0u : (unsigned)c;
@@ -1330,10 +1350,29 @@ __global__ void __launch_bounds__(256) k_hd_pass(int p, const uint8_t* rec, cons
     } else {
       unsigned long long e = want;
       long long c = 0;
-      if (want < (i + 1) * HD_S) c = hd_decode<false>(*T, lut, pay, want, (i + 1) * HD_S, &e, nullptr);
-      W.s[wr][i] = want;
-      W.e[wr][i] = c < 0 ? ~0ull : e;
-      W.c[wr][i] = c < 0 ? 0u : (unsigned)c;
+      bool done = false;
+      if (p == 1 && W.e[rd][i] != ~0ull && want >= i * HD_S) {
+        // decode from the true start until it meets a codeword start of the
+        // first pass (from there both decodes are identical)
+        unsigned long long ps;
+        const unsigned long long bm = W.bmask[i];
+        const long long k = hd_decode<false, false, true>(*T, lut, pay, want, (i + 1) * HD_S, &ps, nullptr, nullptr,
+                                                          i * HD_S, bm);
+        if (k >= 0) {
+          const unsigned long long q = ps - i * HD_S;
+          const unsigned before = __popcll(bm & ((1ull << q) - 1));
+          W.s[wr][i] = want;
+          W.e[wr][i] = W.e[rd][i];
+          W.c[wr][i] = W.c[rd][i] - before + (unsigned)k;
+          done = true;
+        }
+      }
+      if (!done) {
+        if (want < (i + 1) * HD_S) c = hd_decode<false>(*T, lut, pay, want, (i + 1) * HD_S, &e, nullptr);
+        W.s[wr][i] = want;
+        W.e[wr][i] = c < 0 ? ~0ull : e;
+        W.c[wr][i] = c < 0 ? 0u : (unsigned)c;
+      }
       ch = true;
     }
   }
@@ -1439,7 +1478,7 @@ __global__ void k_hd_serial(const uint8_t* rec, const HDTables* T, HDWork W, int
 
 size_t huffman_decode_ws_bytes(unsigned long long max_payload_bytes) {
   const unsigned long long nsub = cdiv(max_payload_bytes * 8, HD_S) + 1;
-  return sizeof(HDTables) + 256 + nsub * (8 * 2 + 8 * 2 + 4 * 2 + 8) + 64 + 256;
+  return sizeof(HDTables) + 256 + nsub * (8 * 2 + 8 * 2 + 4 * 2 + 8 + 8) + 64 + 256;
 }
 
 void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long* len_dev, unsigned long long n,
@@ -1457,6 +1496,8 @@ void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long*
     p += nsub_max * 8;
   }
   W.off = reinterpret_cast<unsigned long long*>(p);
+  p += nsub_max * 8;
+  W.bmask = reinterpret_cast<unsigned long long*>(p);
   p += nsub_max * 8;
   for (int b = 0; b < 2; b++) {
     W.c[b] = reinterpret_cast<unsigned*>(p);
