@@ -522,7 +522,7 @@ __global__ void k_huff_zero(uint32_t* rec_words, DevState* st) {
 
 constexpr int HE_SYMS = 32;  // symbols per thread
 constexpr int HE_TILE = 256 * HE_SYMS;
-constexpr int HE_SMEM_WORDS = HE_TILE * 2 + 2;  // 64 bits per symbol worst case
+constexpr int HE_SMEM_WORDS = HE_TILE / 4 + 64;  // 8 bits/symbol; larger tiles take the global path
 
 // Each tile (8192 symbols) packs its codes MSB-first into a shared-memory bit
 // buffer (smem atomics only where two threads share a word), then streams the
@@ -1194,21 +1194,29 @@ struct OutWriter {
     p++;
     if (!(p & 15)) flush_chunk(p - 16, 16);
   }
+  // n copies of byte b: masked fill of the current 16-byte window, whole
+  // windows as single 16-byte stores
   __device__ __forceinline__ void run(int b, unsigned long long n) {
-    while (n && (p & 15)) {
-      put(b);
-      n--;
-    }
     const uint64_t rep = 0x0101010101010101ull * (uint64_t)b;
-    while (n >= 16) {
-      lo = hi = rep;
-      flush_chunk(p, 16);
-      p += 16;
-      n -= 16;
-    }
     while (n) {
-      put(b);
-      n--;
+      const int k = (int)(p & 15);
+      const int take = n < (unsigned long long)(16 - k) ? (int)n : 16 - k;
+      if (k == 0 && take == 16) {
+        lo = hi = rep;
+        flush_chunk(p, 16);
+      } else {
+        // bytes [k, k+take) of the window
+        const int a = k, e = k + take;
+        const uint64_t mlo = (a < 8) ? ((e >= 8 ? ~0ull : ((1ull << (8 * e)) - 1)) & (~0ull << (8 * a))) : 0ull;
+        const uint64_t mhi = (e > 8) ? ((e >= 16 ? ~0ull : ((1ull << (8 * (e - 8))) - 1)) &
+                                        (a <= 8 ? ~0ull : (~0ull << (8 * (a - 8)))))
+                                     : 0ull;
+        lo |= rep & mlo;
+        hi |= rep & mhi;
+        if (e == 16) flush_chunk(p - k, 16);
+      }
+      p += take;
+      n -= take;
     }
   }
   __device__ void finish() {
