@@ -139,7 +139,16 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     oracle.set_threads(cores)
     S = args.size
-    vals = synth.make("grf", (S, S, S), seed=2025) if args.kind == "grf" else synth.make(args.kind, (S, S, S), seed=2025)
+    # the same input bytes as the GPU arm (generated with torch on the GPU when
+    # one is present; generation is not part of the timed path)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            vals = synth.make_device(args.kind, (S, S, S), seed=2025).cpu().numpy()
+        else:
+            raise RuntimeError
+    except Exception:
+        vals = synth.make(args.kind, (S, S, S), seed=2025)
     n = vals.size
     times = []
     for i in range(args.warmup + args.steps):
@@ -270,8 +279,14 @@ def run_ours(args):
         ms = cand[dom]
         ab = algo_bytes(dom, n, 4, archive_len)
         ach = ab / (ms / 1e3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+                traffic = json.load(fh).get(dom)
+        except Exception:
+            pass
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 2), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": None, "algo_bytes": int(ab), "ms": round(ms, 4),
+                "frac": round(ach / peak, 4), "traffic": traffic, "algo_bytes": int(ab), "ms": round(ms, 4),
                 "peak_kind": peak_kind}
 
     line = {
