@@ -93,7 +93,7 @@ __device__ __forceinline__ long long slot(const LevelGeom& g, long long P0, long
 // in the local index, so they are evaluated as base + i*stride; the global
 // loads of a thread's points are issued up front (one batch per class) so
 // their latency overlaps.
-template <class TL, int CLS, int AXM, int HALO, bool LINEAR, bool DEC, typename T>
+template <class TL, int CLS, int AXM, int HALO, bool LINEAR, bool DEC, typename T, bool INT>
 __device__ __forceinline__ void process_class(const LvArgs& A, const CtaCtx& c, double* sm, unsigned* shist,
                                               bool& bad, bool& nf) {
   double* stage = sm + TL::total();  // per-class load staging (after the class arrays)
@@ -143,7 +143,8 @@ __device__ __forceinline__ void process_class(const LvArgs& A, const CtaCtx& c, 
     for (int it = 0; it < ITERS; it++) {
       const int idx = it * LV_THREADS + threadIdx.x;
       const int i2 = idx % n2, i1 = (idx / n2) % n1, i0 = idx / (n2 * n1);
-      const bool live = idx < total && i0 >= ilo0 && i0 < ihi0 && i1 >= ilo1 && i1 < ihi1 && i2 >= ilo2 && i2 < ihi2;
+      const bool live = INT ? idx < total
+                            : idx < total && i0 >= ilo0 && i0 < ihi0 && i1 >= ilo1 && i1 < ihi1 && i2 >= ilo2 && i2 < ihi2;
       if (idx < total) {
         if (!DEC) {
           const T* src = reinterpret_cast<const T*>(A.field) + (live ? lin0 + i0 * kl0 + i1 * kl1 + i2 * kl2 : 0);
@@ -161,7 +162,8 @@ __device__ __forceinline__ void process_class(const LvArgs& A, const CtaCtx& c, 
     for (int it = 0; it < ITERS; it++) {
       const int idx = it * LV_THREADS + threadIdx.x;
       const int i2 = idx % n2, i1 = (idx / n2) % n1, i0 = idx / (n2 * n1);
-      const bool live = idx < total && i0 >= ilo0 && i0 < ihi0 && i1 >= ilo1 && i1 < ihi1 && i2 >= ilo2 && i2 < ihi2;
+      const bool live = INT ? idx < total
+                            : idx < total && i0 >= ilo0 && i0 < ihi0 && i1 >= ilo1 && i1 < ihi1 && i2 >= ilo2 && i2 < ihi2;
       const int l[3] = {lo0 + i0, lo1 + i1, lo2 + i2};
       bool owned = true;
 #pragma unroll
@@ -181,7 +183,8 @@ __device__ __forceinline__ void process_class(const LvArgs& A, const CtaCtx& c, 
           const int step = a == 0 ? s0 : (a == 1 ? s1 : 1);
           const double* b = sm + TL::off(cn) + l[0] * s0 + l[1] * s1 + l[2];
           const int Pa = a == 0 ? (int)P00 + 2 * i0 : (a == 1 ? (int)P10 + 2 * i1 : (int)P20 + 2 * i2);
-          const int cls = classify(Pa, c.D[a], 1, LINEAR);
+          // interior tiles: every stencil is the full one (cubic / linear mid-point)
+          const int cls = INT ? (LINEAR ? ST_MID : ST_CUBIC) : classify(Pa, c.D[a], 1, LINEAR);
           pv[k] = cls == ST_CUBIC ? apply_stencil(ST_CUBIC, b[0], b[step], b[2 * step], b[3 * step])
                                   : apply_stencil(cls, b[0], b[step], b[2 * step], b[3 * step]);
           ov[k] = stencil_order(cls);
@@ -244,51 +247,51 @@ __device__ __forceinline__ void process_class(const LvArgs& A, const CtaCtx& c, 
 
 // multidim (predictor.py:282-296): phases by number of odd axes, every even
 // axis carries the halo, a class interpolates along all its odd axes
-template <class TL, bool LINEAR, bool DEC, typename T>
+template <class TL, bool LINEAR, bool DEC, typename T, bool INT>
 __device__ __forceinline__ void run_multidim(const LvArgs& A, const CtaCtx& c, double* sm, unsigned* sh, bool& bad, bool& nf) {
-  process_class<TL, 1, 1, 6, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
-  process_class<TL, 2, 2, 5, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
-  process_class<TL, 4, 4, 3, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
+  process_class<TL, 1, 1, 6, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
+  process_class<TL, 2, 2, 5, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
+  process_class<TL, 4, 4, 3, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
   __syncthreads();
-  process_class<TL, 3, 3, 4, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
-  process_class<TL, 5, 5, 2, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
-  process_class<TL, 6, 6, 1, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
+  process_class<TL, 3, 3, 4, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
+  process_class<TL, 5, 5, 2, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
+  process_class<TL, 6, 6, 1, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
   __syncthreads();
-  process_class<TL, 7, 7, 0, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
+  process_class<TL, 7, 7, 0, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
 }
 
 // seq1d (predictor.py:267-280) with axis order (O0, O1, O2): pass k predicts
 // points odd on Ok along Ok only; halo on the axes of later passes
-template <class TL, int O0, int O1, int O2, bool LINEAR, bool DEC, typename T>
+template <class TL, int O0, int O1, int O2, bool LINEAR, bool DEC, typename T, bool INT>
 __device__ __forceinline__ void run_seq1d(const LvArgs& A, const CtaCtx& c, double* sm, unsigned* sh, bool& bad, bool& nf) {
   constexpr int b0 = 1 << O0, b1 = 1 << O1, b2 = 1 << O2;
-  process_class<TL, b0, b0, b1 | b2, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
+  process_class<TL, b0, b0, b1 | b2, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
   __syncthreads();
-  process_class<TL, b1, b1, b2, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
-  process_class<TL, b0 | b1, b1, b2, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
+  process_class<TL, b1, b1, b2, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
+  process_class<TL, b0 | b1, b1, b2, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
   __syncthreads();
-  process_class<TL, b2, b2, 0, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
-  process_class<TL, b0 | b2, b2, 0, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
-  process_class<TL, b1 | b2, b2, 0, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
-  process_class<TL, 7, b2, 0, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
+  process_class<TL, b2, b2, 0, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
+  process_class<TL, b0 | b2, b2, 0, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
+  process_class<TL, b1 | b2, b2, 0, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
+  process_class<TL, 7, b2, 0, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
 }
 
-template <class TL, bool LINEAR, bool DEC, typename T>
+template <class TL, bool LINEAR, bool DEC, typename T, bool INT>
 __device__ __forceinline__ void run_seq1d_any(int order_id, const LvArgs& A, const CtaCtx& c, double* sm, unsigned* sh, bool& bad, bool& nf) {
   if (TL::big(2)) {
     switch (order_id) {
-      case 0: run_seq1d<TL, 0, 1, 2, LINEAR, DEC, T>(A, c, sm, sh, bad, nf); break;
-      case 1: run_seq1d<TL, 0, 2, 1, LINEAR, DEC, T>(A, c, sm, sh, bad, nf); break;
-      case 2: run_seq1d<TL, 1, 0, 2, LINEAR, DEC, T>(A, c, sm, sh, bad, nf); break;
-      case 3: run_seq1d<TL, 1, 2, 0, LINEAR, DEC, T>(A, c, sm, sh, bad, nf); break;
-      case 4: run_seq1d<TL, 2, 0, 1, LINEAR, DEC, T>(A, c, sm, sh, bad, nf); break;
-      default: run_seq1d<TL, 2, 1, 0, LINEAR, DEC, T>(A, c, sm, sh, bad, nf); break;
+      case 0: run_seq1d<TL, 0, 1, 2, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf); break;
+      case 1: run_seq1d<TL, 0, 2, 1, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf); break;
+      case 2: run_seq1d<TL, 1, 0, 2, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf); break;
+      case 3: run_seq1d<TL, 1, 2, 0, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf); break;
+      case 4: run_seq1d<TL, 2, 0, 1, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf); break;
+      default: run_seq1d<TL, 2, 1, 0, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf); break;
     }
   } else {  // d2 == 1 sorts last
     if (order_id == 2)
-      run_seq1d<TL, 1, 0, 2, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
+      run_seq1d<TL, 1, 0, 2, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
     else
-      run_seq1d<TL, 0, 1, 2, LINEAR, DEC, T>(A, c, sm, sh, bad, nf);
+      run_seq1d<TL, 0, 1, 2, LINEAR, DEC, T, INT>(A, c, sm, sh, bad, nf);
   }
 }
 
@@ -342,12 +345,31 @@ __global__ void __launch_bounds__(LV_THREADS, 3) k_level_tiled(LvArgs A, int ord
   }
   __syncthreads();
   const int cfg = A.st->cfg[g.level - 1] & 3;
+  // interior tile: all computed points (tile + halo) exist and every stencil is complete
+  bool interior = true;
+  for (int a = 0; a < 3; a++)
+    if (TL::big(a)) {
+      const int P0 = tix[a] * TL::t(a);
+      interior &= P0 >= 2 && P0 + TL::t(a) + 3 <= c.D[a];
+    }
   bool bad = false, nf = nf0;
   switch (cfg) {
-    case 0: run_multidim<TL, false, DEC, T>(A, c, sm, shist, bad, nf); break;
-    case 1: run_multidim<TL, true, DEC, T>(A, c, sm, shist, bad, nf); break;
-    case 2: run_seq1d_any<TL, false, DEC, T>(order_id, A, c, sm, shist, bad, nf); break;
-    default: run_seq1d_any<TL, true, DEC, T>(order_id, A, c, sm, shist, bad, nf); break;
+    case 0:
+      if (interior) run_multidim<TL, false, DEC, T, true>(A, c, sm, shist, bad, nf);
+      else run_multidim<TL, false, DEC, T, false>(A, c, sm, shist, bad, nf);
+      break;
+    case 1:
+      if (interior) run_multidim<TL, true, DEC, T, true>(A, c, sm, shist, bad, nf);
+      else run_multidim<TL, true, DEC, T, false>(A, c, sm, shist, bad, nf);
+      break;
+    case 2:
+      if (interior) run_seq1d_any<TL, false, DEC, T, true>(order_id, A, c, sm, shist, bad, nf);
+      else run_seq1d_any<TL, false, DEC, T, false>(order_id, A, c, sm, shist, bad, nf);
+      break;
+    default:
+      if (interior) run_seq1d_any<TL, true, DEC, T, true>(order_id, A, c, sm, shist, bad, nf);
+      else run_seq1d_any<TL, true, DEC, T, false>(order_id, A, c, sm, shist, bad, nf);
+      break;
   }
   if (DEC && __any_sync(0xffffffffu, nf) && (threadIdx.x & 31) == 0) raise_flag(A.st, F_NONFINITE);
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) raise_flag(A.st, DEC ? F_ORPHAN : F_NONFINITE);
