@@ -122,19 +122,22 @@ __device__ __forceinline__ void process_class(const LvArgs& A, const CtaCtx& c, 
     const int ilo2 = -xb2, ihi2 = ((c.D[2] - odd2 + 1) >> 1) - xb2;
     // affine maps at i = 0 (P may be negative there; the maps stay linear)
     const LevelGeom& g = A.g;  // kernel-parameter constants
+    // (the tiled kernels only run when every element index fits in int32,
+    // so all per-point address arithmetic below is 32-bit)
     const long long P00 = 2ll * xb0 + odd0, P10 = 2ll * xb1 + odd1, P20 = 2ll * xb2 + odd2;
-    const long long lin0 = ((P00 * g.s) * g.d[1] + P10 * g.s) * g.d[2] + P20 * g.s;
-    const long long kl0 = g.kl[0], kl1 = g.kl[1], kl2 = g.kl[2];
-    long long sl0 = g.prefix + (P00 * g.D[1] + P10) * g.D[2] + P20 - ((P00 + 1) >> 1) * g.eyez;
+    const int lin0 = (int)(((P00 * g.s) * g.d[1] + P10 * g.s) * g.d[2] + P20 * g.s);
+    const int kl0 = (int)g.kl[0], kl1 = (int)g.kl[1], kl2 = (int)g.kl[2];
+    long long sl0l = g.prefix + (P00 * g.D[1] + P10) * g.D[2] + P20 - ((P00 + 1) >> 1) * g.eyez;
     if (!odd0) {
-      sl0 -= ((P10 + 1) >> 1) * g.ez;
-      if (!odd1) sl0 -= (P20 + 1) >> 1;
+      sl0l -= ((P10 + 1) >> 1) * g.ez;
+      if (!odd1) sl0l -= (P20 + 1) >> 1;
     }
-    const long long ks0 = g.ks0;
-    const long long ks1 = odd0 ? g.ks1_odd0 : g.ks1_even0;
-    constexpr long long ks2 = (odd0 || odd1) ? 2 : 1;
-    const long long ke0 = g.ke[0], ke1 = g.ke[1], ke2 = g.ke[2];
-    const long long E0 = (((P00 * g.s) >> 1) * g.Ed[1] + ((P10 * g.s) >> 1)) * g.Ed[2] + ((P20 * g.s) >> 1);
+    const int sl0 = (int)sl0l;
+    const int ks0 = (int)g.ks0;
+    const int ks1 = (int)(odd0 ? g.ks1_odd0 : g.ks1_even0);
+    constexpr int ks2 = (odd0 || odd1) ? 2 : 1;
+    const int ke0 = (int)g.ke[0], ke1 = (int)g.ke[1], ke2 = (int)g.ke[2];
+    const int E0 = (int)((((P00 * g.s) >> 1) * g.Ed[1] + ((P10 * g.s) >> 1)) * g.Ed[2] + ((P20 * g.s) >> 1));
     // ---- phase A: issue all of this thread's global loads (independent, so
     // their latency overlaps) into a per-thread slot of the staging area
     T* stf = reinterpret_cast<T*>(stage);
@@ -150,7 +153,7 @@ __device__ __forceinline__ void process_class(const LvArgs& A, const CtaCtx& c, 
           const T* src = reinterpret_cast<const T*>(A.field) + (live ? lin0 + i0 * kl0 + i1 * kl1 + i2 * kl2 : 0);
           cp_async<sizeof(T)>(stf + idx, src, live);
         } else {
-          const long long sl = live ? sl0 + i0 * ks0 + i1 * ks1 + i2 * ks2 : 0;
+          const int sl = live ? sl0 + i0 * ks0 + i1 * ks1 + i2 * ks2 : 0;
           const uintptr_t ad = reinterpret_cast<uintptr_t>(A.seq + sl) & ~uintptr_t(3);
           cp_async<4>(stc + idx, reinterpret_cast<const void*>(ad), live);
         }
@@ -197,7 +200,7 @@ __device__ __forceinline__ void process_class(const LvArgs& A, const CtaCtx& c, 
           code = quantize_fast<sizeof(T) == 4>(o, pred, c.eb, c.two_eb, c.inv_two_eb, &r);
           if (owned) {
             A.seq[sl0 + i0 * ks0 + i1 * ks1 + i2 * ks2] = (uint8_t)code;
-            const long long lin = lin0 + i0 * kl0 + i1 * kl1 + i2 * kl2;
+            const int lin = lin0 + i0 * kl0 + i1 * kl1 + i2 * kl2;
             if (code == 0) atomicOr(&A.obm[lin >> 5], 1u << (lin & 31));
             bad |= !isfinite(o);
             if (A.g.level >= 2) A.E[E0 + i0 * ke0 + i1 * ke1 + i2 * ke2] = r;
@@ -208,7 +211,7 @@ __device__ __forceinline__ void process_class(const LvArgs& A, const CtaCtx& c, 
           if (code != 0) {
             r = dequantize(pred, c.two_eb, code);
           } else {
-            const unsigned long long lin = (unsigned long long)(lin0 + i0 * kl0 + i1 * kl1 + i2 * kl2);
+            const unsigned long long lin = (unsigned long long)(unsigned)(lin0 + i0 * kl0 + i1 * kl1 + i2 * kl2);
             unsigned long long a0 = 0, a1 = c.ocount;
             while (a0 < a1) {
               const unsigned long long mid = (a0 + a1) >> 1;
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(LV_THREADS, 3) k_level_tiled(LvArgs A, int ord
       const int l2 = idx % e2, l1 = (idx / e2) % e1, l0 = idx / (e2 * e1);
       const int h0 = c.hb0[0] - TL::eoff(0) + l0, h1 = c.hb0[1] - TL::eoff(1) + l1, h2 = c.hb0[2] - TL::eoff(2) + l2;
       const bool ok = h0 >= 0 && 2 * h0 < c.D[0] && h1 >= 0 && 2 * h1 < c.D[1] && h2 >= 0 && 2 * h2 < c.D[2];
-      const double* src = A.E + (ok ? (((long long)h0 * c.s) * c.e1 + (long long)h1 * c.s) * c.e2 + (long long)h2 * c.s : 0);
+      const double* src = A.E + (ok ? ((h0 * (int)c.s) * (int)c.e1 + h1 * (int)c.s) * (int)c.e2 + h2 * (int)c.s : 0);
       cp_async<8>(sm + idx, src, ok);
     }
     cp_async_wait_all();
@@ -395,6 +398,7 @@ template <bool DEC>
 static inline bool launch_tiled(LevelGeom g, const LvArgs& base, int prec, cudaStream_t s) {
   const bool b0 = g.d[0] > 1, b1 = g.d[1] > 1, b2 = g.d[2] > 1;
   LvArgs A = base;
+  if (g.d[0] * g.d[1] * g.d[2] >= (1ll << 31) - (1ll << 24)) return false;  // 32-bit indexing only
   int kind;
   if (b0 && b1 && b2)
     kind = 3;

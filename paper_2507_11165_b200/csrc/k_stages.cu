@@ -997,7 +997,25 @@ struct HDTables {
   int first_rank[64], count[64];
   uint8_t syms[256];
   uint16_t lut[1 << HD_K];  // (len << 8) | sym, 0 = none
+  // multi-symbol table over the same K-bit window: up to 4 complete codewords
+  uint32_t msym[1 << HD_K];  // packed symbols, first in the low byte
+  uint8_t mmeta[1 << HD_K];  // count | bits << 3
 };
+
+// shared-memory copy of the decode tables used per symbol
+struct HDShared {
+  uint16_t lut[1 << HD_K];
+  uint32_t msym[1 << HD_K];
+  uint8_t mmeta[1 << HD_K];
+};
+
+__device__ __forceinline__ void hd_load_shared(HDShared* S, const HDTables* T) {
+  for (int i = threadIdx.x; i < (1 << HD_K); i += blockDim.x) {
+    S->lut[i] = T->lut[i];
+    S->msym[i] = T->msym[i];
+    S->mmeta[i] = T->mmeta[i];
+  }
+}
 
 struct HDWork {  // per pass: start, end, count per subsequence
   unsigned long long* s[2];
@@ -1122,6 +1140,26 @@ __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsi
     }
     T->lut[e] = v;
   }
+  __syncthreads();
+  // multi-symbol entries: greedy decode of the codewords wholly inside the window
+  for (int e = t; e < (1 << HD_K); e += 256) {
+    uint32_t packed = 0;
+    int n = 0, used = 0;
+    if (e < (1 << K)) {
+      while (n < 4) {
+        const int rem = K - used;
+        if (rem <= 0) break;
+        const uint16_t v = T->lut[((unsigned)e << used) & ((1u << K) - 1)];
+        const int L = v >> 8;
+        if (!v || L > rem) break;
+        packed |= (uint32_t)(v & 0xFF) << (8 * n);
+        n++;
+        used += L;
+      }
+    }
+    T->msym[e] = packed;
+    T->mmeta[e] = (uint8_t)(n | (used << 3));
+  }
   if (t == 0) {
     T->run_sym = (T->count[1] > 0 && T->first_code[1] == 0) ? T->syms[T->first_rank[1]] : -1;
     __threadfence();
@@ -1229,7 +1267,7 @@ struct OutWriter {
 // SYNC: stop early at the first codeword start p with (p - sbase) < 64 and
 //       bit (p - sbase) of sync_mask set (*endp = p).
 template <bool EMIT, bool MASK = false, bool SYNC = false>
-__device__ long long hd_decode(const HDTables& T, const uint16_t* lut, const uint8_t* pay, unsigned long long start,
+__device__ long long hd_decode(const HDTables& T, const HDShared* S, const uint8_t* pay, unsigned long long start,
                                unsigned long long stop, unsigned long long* endp, OutWriter* ow,
                                unsigned long long* mask = nullptr, unsigned long long sbase = 0,
                                unsigned long long sync_mask = 0) {
@@ -1270,7 +1308,26 @@ __device__ long long hd_decode(const HDTables& T, const uint16_t* lut, const uin
       br.consume((int)z);
       continue;
     }
-    const uint16_t e = lut[br.buf >> (64 - K)];
+    const unsigned key = (unsigned)(br.buf >> (64 - K));
+    if (!SYNC && (!MASK || pos - start >= 64)) {  // several short codewords at once, all starting before lim
+      const uint8_t mm = S->mmeta[key];
+      const int n = mm & 7, b = mm >> 3;
+      if (n >= 2 && pos + b <= lim) {
+        if (EMIT) {
+          const uint32_t pk = S->msym[key];
+          for (int q = 0; q < n; q++) {
+            const int sy = (pk >> (8 * q)) & 0xFF;
+            ow->put(sy);
+            ow->zeros += sy == 0;
+          }
+        }
+        pos += b;
+        cnt += n;
+        br.consume(b);
+        continue;
+      }
+    }
+    const uint16_t e = S->lut[key];
     int L, sym;
     if (e) {
       L = e >> 8;
@@ -1311,9 +1368,9 @@ __device__ long long hd_decode(const HDTables& T, const uint16_t* lut, const uin
 }
 
 __global__ void __launch_bounds__(256) k_hd_first(const uint8_t* rec, const HDTables* T, HDWork W, DevState* st) {
-  __shared__ uint16_t lut[1 << HD_K];
+  __shared__ HDShared S;
   if (!T->ok) return;
-  for (int i = threadIdx.x; i < (1 << HD_K); i += blockDim.x) lut[i] = T->lut[i];
+  hd_load_shared(&S, T);
   __syncthreads();
   const unsigned long long nsub = T->nsub;
   const uint8_t* pay = rec + T->pay_off;
@@ -1321,7 +1378,7 @@ __global__ void __launch_bounds__(256) k_hd_first(const uint8_t* rec, const HDTa
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned long long s0 = i * HD_S;
     unsigned long long e, m = 0;
-    const long long c = hd_decode<false, true>(*T, lut, pay, s0, s0 + HD_S, &e, nullptr, &m);
+    const long long c = hd_decode<false, true>(*T, &S, pay, s0, s0 + HD_S, &e, nullptr, &m);
     W.bmask[i] = m;
     W.s[0][i] = s0;
     W.e[0][i] = c < 0 ? ~0ull : e;  // error end never matches a successor start
@@ -1331,7 +1388,7 @@ __global__ void __launch_bounds__(256) k_hd_first(const uint8_t* rec, const HDTa
 
 // pass p: read buffers (p-1)&1, write p&1
 __global__ void __launch_bounds__(256) k_hd_pass(int p, const uint8_t* rec, const HDTables* T, HDWork W) {
-  __shared__ uint16_t lut[1 << HD_K];
+  __shared__ HDShared S;
   if (!T->ok) return;
   const int rd = (p - 1) & 1, wr = p & 1;
   const unsigned long long nsub = T->nsub;
@@ -1344,7 +1401,7 @@ __global__ void __launch_bounds__(256) k_hd_pass(int p, const uint8_t* rec, cons
     }
     return;
   }
-  for (int i = threadIdx.x; i < (1 << HD_K); i += blockDim.x) lut[i] = T->lut[i];
+  hd_load_shared(&S, T);
   __syncthreads();
   const uint8_t* pay = rec + T->pay_off;
   bool ch = false;
@@ -1364,7 +1421,7 @@ __global__ void __launch_bounds__(256) k_hd_pass(int p, const uint8_t* rec, cons
         // first pass (from there both decodes are identical)
         unsigned long long ps;
         const unsigned long long bm = W.bmask[i];
-        const long long k = hd_decode<false, false, true>(*T, lut, pay, want, (i + 1) * HD_S, &ps, nullptr, nullptr,
+        const long long k = hd_decode<false, false, true>(*T, &S, pay, want, (i + 1) * HD_S, &ps, nullptr, nullptr,
                                                           i * HD_S, bm);
         if (k >= 0) {
           const unsigned long long q = ps - i * HD_S;
@@ -1376,7 +1433,7 @@ __global__ void __launch_bounds__(256) k_hd_pass(int p, const uint8_t* rec, cons
         }
       }
       if (!done) {
-        if (want < (i + 1) * HD_S) c = hd_decode<false>(*T, lut, pay, want, (i + 1) * HD_S, &e, nullptr);
+        if (want < (i + 1) * HD_S) c = hd_decode<false>(*T, &S, pay, want, (i + 1) * HD_S, &e, nullptr);
         W.s[wr][i] = want;
         W.e[wr][i] = c < 0 ? ~0ull : e;
         W.c[wr][i] = c < 0 ? 0u : (unsigned)c;
@@ -1433,10 +1490,10 @@ __global__ void __launch_bounds__(256) k_hd_scan(const HDTables* T, HDWork W, in
 
 __global__ void __launch_bounds__(256) k_hd_emit(const uint8_t* rec, const HDTables* T, HDWork W, int fin,
                                                  uint8_t* out, DevState* st) {
-  __shared__ uint16_t lut[1 << HD_K];
+  __shared__ HDShared S;
   if (!T->ok) return;
   if (st->flags & F_STAGE) return;
-  for (int i = threadIdx.x; i < (1 << HD_K); i += blockDim.x) lut[i] = T->lut[i];
+  hd_load_shared(&S, T);
   __syncthreads();
   const unsigned long long nsub = T->nsub;
   const uint8_t* pay = rec + T->pay_off;
@@ -1453,7 +1510,7 @@ __global__ void __launch_bounds__(256) k_hd_emit(const uint8_t* rec, const HDTab
     OutWriter ow;
     ow.init(out, W.off[i]);
     unsigned long long e;
-    const long long c = hd_decode<true>(*T, lut, pay, s0, (i + 1) * HD_S, &e, &ow);
+    const long long c = hd_decode<true>(*T, &S, pay, s0, (i + 1) * HD_S, &e, &ow);
     ow.finish();
     zeros += ow.zeros;
     bad |= c < 0;
@@ -1477,7 +1534,8 @@ __global__ void k_hd_serial(const uint8_t* rec, const HDTables* T, HDWork W, int
     if (want == W.s[fin][i]) continue;
     unsigned long long e = want;
     long long c = 0;
-    if (want < (i + 1) * HD_S) c = hd_decode<false>(*T, T->lut, pay, want, (i + 1) * HD_S, &e, nullptr);
+    if (want < (i + 1) * HD_S)
+      c = hd_decode<false>(*T, reinterpret_cast<const HDShared*>(T->lut), pay, want, (i + 1) * HD_S, &e, nullptr);
     W.s[fin][i] = want;
     W.e[fin][i] = c < 0 ? ~0ull : e;
     W.c[fin][i] = c < 0 ? 0u : (unsigned)c;
