@@ -237,6 +237,25 @@ void bind_chain(uint8_t* base, const size_t offs[9], unsigned long long max_word
 
 unsigned long long lb_entries(unsigned long long items, unsigned long long tile) { return 2 + cdiv(items, tile); }
 
+// Small host->device uploads go through the context's pinned buffer so the
+// copies stay asynchronous (a pageable cudaMemcpyAsync would block the host
+// until the stream drains).  Region [8192, pinned_size) is bump-allocated per
+// call; every call ends with a stream synchronise, so reuse is safe.
+struct PinnedUp {
+  hb_ctx* ctx;
+  size_t off = 8192;
+  int put(void* dev, const void* src, size_t n, cudaStream_t s) {
+    if (off + n > ctx->pinned_size) {
+      cudaError_t e = cudaMemcpy(dev, src, n, cudaMemcpyHostToDevice);  // oversized: synchronous fallback
+      return e == cudaSuccess ? 0 : set_err(ctx, HB_ECUDA, "upload: %s", cudaGetErrorString(e));
+    }
+    memcpy(ctx->pinned + off, src, n);
+    cudaError_t e = cudaMemcpyAsync(dev, ctx->pinned + off, n, cudaMemcpyHostToDevice, s);
+    off += (n + 255) & ~size_t(255);
+    return e == cudaSuccess ? 0 : set_err(ctx, HB_ECUDA, "upload: %s", cudaGetErrorString(e));
+  }
+};
+
 struct HostStatus {
   double eb;
   uint32_t flags, detail;
@@ -515,7 +534,7 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
   const size_t lb_bytes = (lb_oc + lb_he + 4 * lb_c1 + 4 * lb_c2) * 8;
   rc = ensure_arena(ctx, L.off);
   if (rc) return rc;
-  rc = ensure_pinned(ctx, 1 << 16);
+  rc = ensure_pinned(ctx, 8192 + org.size() * 8 + 4096);
   if (rc) return rc;
   uint8_t* base = ctx->arena;
   DevState* st = reinterpret_cast<DevState*>(base + o_st);
@@ -542,9 +561,10 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
   CU(cudaMemsetAsync(st, 0, sizeof(DevState), s));
   CU(cudaMemsetAsync(obm, 0, cdiv(N, 32) * 4 + 64, s));
   CU(cudaMemsetAsync(lb, 0, lb_bytes, s));
-  CU(cudaMemcpyAsync(d_org, org.data(), org.size() * 8, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(cb1.table, t1.data(), 8 * sizeof(void*), cudaMemcpyHostToDevice, s));
-  if (mode == 0) CU(cudaMemcpyAsync(cb2.table, t2.data(), 8 * sizeof(void*), cudaMemcpyHostToDevice, s));
+  PinnedUp up{ctx};
+  if ((rc = up.put(d_org, org.data(), org.size() * 8, s))) return rc;
+  if ((rc = up.put(cb1.table, t1.data(), 8 * sizeof(void*), s))) return rc;
+  if (mode == 0 && (rc = up.put(cb2.table, t2.data(), 8 * sizeof(void*), s))) return rc;
   ctx->nev = 0;
   ctx->mark("start");
   // 1) error bound (field.py:135-142)
@@ -604,7 +624,7 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
     for (int a = 0; a < 3; a++)
       for (int i = 0; i < 8; i++) h.b[14 + 8 * a + i] = (uint8_t)(dims[a] >> (8 * i));
     uint8_t* d_h = reinterpret_cast<uint8_t*>(&st->scratch[8]);  // 46 bytes inside DevState scratch
-    CU(cudaMemcpyAsync(d_h, h.b, 46, cudaMemcpyHostToDevice, s));
+    if ((rc = up.put(d_h, h.b, 46, s))) return rc;
     ctx->mark("lossless");
     launch_archive_tail_impl(arch, obase, prec, seq, N, d_h, na, st, s, &nl);
     ctx->mark("archive");
@@ -1017,8 +1037,9 @@ int hb_stage_encode(hb_ctx* ctx, int stage, int width, const void* in, size_t n,
   int nl = 0;
   CU(cudaMemsetAsync(st, 0, sizeof(DevState), s));
   CU(cudaMemsetAsync(base + o_lb, 0, lbn * 8 * 12, s));
-  CU(cudaMemcpyAsync(cb1.table, t1.data(), 8 * sizeof(void*), cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(cb2.table, t2.data(), 8 * sizeof(void*), cudaMemcpyHostToDevice, s));
+  PinnedUp up{ctx};
+  if ((rc = up.put(cb1.table, t1.data(), 8 * sizeof(void*), s))) return rc;
+  if ((rc = up.put(cb2.table, t2.data(), 8 * sizeof(void*), s))) return rc;
   if (n) CU(cudaMemcpyAsync(base + o_in, in, n, cudaMemcpyDefault, s));
   k_set_u64<<<1, 1, 0, s>>>(&st->seq_len, n);
   nl++;

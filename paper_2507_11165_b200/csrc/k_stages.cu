@@ -72,6 +72,30 @@ struct MemSrc {  // plain bytes
       if (o + k < len) v |= (uint64_t)p[o + k] << (8 * k);
     return v;
   }
+  // words [i0, i0+32) (i0 % 32 == 0), zero past the end
+  __device__ void load32(unsigned long long i0, uint64_t* v) const {
+    const unsigned long long o = i0 * w;
+    if (o + 32ull * w <= len && !((uintptr_t)(p + o) & 15)) {
+      const uint4* q = reinterpret_cast<const uint4*>(p + o);
+      if (w == 1) {
+        const uint4 a = q[0], b = q[1];
+        const uint32_t u[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int j = 0; j < 32; j++) v[j] = (u[j >> 2] >> (8 * (j & 3))) & 0xFF;
+        return;
+      }
+      if (w == 4) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          const uint4 a = q[k];
+          v[4 * k] = a.x, v[4 * k + 1] = a.y, v[4 * k + 2] = a.z, v[4 * k + 3] = a.w;
+        }
+        return;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 32; j++) v[j] = word(i0 + j);
+  }
 };
 
 // TCMS(width tw) record of a byte buffer, read as bytes (feeds RZE1 in CR)
@@ -96,6 +120,31 @@ struct TcmsSrc {
     return (zz(u, tw) >> (8 * r)) & 0xFF;
   }
   __device__ unsigned long long len() const { return 10 + cdiv(n, tw) * tw; }
+  __device__ void load32(unsigned long long i0, uint64_t* v) const {
+    if (tw == 8 && i0 >= 32) {  // bytes [i0, i0+32) = words (i0-10)/8 .. +4 of zz(data)
+      const unsigned long long q0 = (i0 - 10) >> 3;  // (i0-10) % 8 == 6
+      uint64_t z[5];
+#pragma unroll
+      for (int k = 0; k < 5; k++) {
+        const unsigned long long o = (q0 + k) * 8;
+        uint64_t u = 0;
+        if (o + 8 <= n)
+          u = *reinterpret_cast<const uint64_t*>(p + o);
+        else
+          for (int b = 0; b < 8; b++)
+            if (o + b < n) u |= (uint64_t)p[o + b] << (8 * b);
+        z[k] = o < n ? zz(u, 8) : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; j++) {
+        const int b = 6 + j;  // byte position from word q0
+        v[j] = (z[b >> 3] >> (8 * (b & 7))) & 0xFF;
+      }
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; j++) v[j] = word(i0 + j);
+  }
 };
 
 // BIT1(TCMS1(seq)) record bytes (feeds RRE1 in TP): stages.py:430-431
@@ -141,6 +190,22 @@ struct TpSrc {
     return bit_plane(tcms_group(t), (int)((j - 10) & 7));
   }
   __device__ unsigned long long len() const { return 10 + cdiv(n + 10, 8) * 8; }
+  __device__ void load32(unsigned long long i0, uint64_t* v) const {
+    if (i0 >= 32) {  // record bytes [i0, i0+32) = planes of tiles (i0-10)/8 .. +4
+      const unsigned long long t0 = (i0 - 10) >> 3;  // (i0-10) % 8 == 6
+      uint64_t g[5];
+#pragma unroll
+      for (int k = 0; k < 5; k++) g[k] = tcms_group(t0 + k);
+#pragma unroll
+      for (int j = 0; j < 32; j++) {
+        const int b = 6 + j;
+        v[j] = bit_plane(g[b >> 3], b & 7);
+      }
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; j++) v[j] = word(i0 + j);
+  }
 };
 
 // ------------------------------------------------------- reducer encode
@@ -160,59 +225,49 @@ __device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage, i
     __syncthreads();
     const unsigned long long tile = tile_sh;
     if (tile >= ntiles) break;
-    const unsigned long long w0 = tile * RD_TILE + (unsigned long long)wid * 1024;
-    uint32_t my_mask = 0;  // lane k keeps the keep-mask of step k
-    unsigned cnt = 0;
-    uint64_t prev_last = 0;
-    for (int k = 0; k < 32; k++) {
-      const unsigned long long i = w0 + k * 32 + lane;
-      if (w0 + k * 32 >= nw) break;  // warp-uniform
-      const bool in = i < nw;
-      const uint64_t v = in ? src.word(i) : 0;
-      bool keep;
-      if (stage == 2) {
-        uint64_t pv = __shfl_up_sync(0xffffffffu, v, 1);
-        if (lane == 0) pv = k == 0 ? (i > 0 ? src.word(i - 1) : ~v) : prev_last;
-        keep = in && (i == 0 || v != pv);
-      } else {
-        keep = in && v != 0;
+    // each lane owns 32 consecutive words: independent loads, one bitmap word
+    const unsigned long long i0 = tile * RD_TILE + (unsigned long long)wid * 1024 + (unsigned long long)lane * 32;
+    uint64_t v[32];
+    uint32_t mask = 0;
+    if (i0 < nw) {
+      src.load32(i0, v);
+      uint64_t prev = 0;
+      if (stage == 2) prev = i0 > 0 ? src.word(i0 - 1) : ~v[0];
+#pragma unroll
+      for (int j = 0; j < 32; j++) {
+        const bool in = i0 + j < nw;
+        const bool keep = in && (stage == 2 ? (i0 + j == 0 || v[j] != (j ? v[j - 1] : prev)) : v[j] != 0);
+        mask |= (uint32_t)keep << (31 - j);  // word i0 at the MSB (np.packbits order)
       }
-      prev_last = __shfl_sync(0xffffffffu, v, 31);
-      const uint32_t m = __ballot_sync(0xffffffffu, keep);
-      if (lane == k) my_mask = m;
-      cnt += __popc(m);
-      if (lane == 0) {
-        const uint32_t be = __brev(m);  // word 0 at the MSB (np.packbits order)
-        *reinterpret_cast<uint32_t*>(bitmap + (w0 + k * 32) / 8) = __byte_perm(be, 0, 0x0123);
-      }
+      *reinterpret_cast<uint32_t*>(bitmap + i0 / 8) = __byte_perm(mask, 0, 0x0123);
     }
+    const unsigned c = __popc(mask);
+    const unsigned incl = warp_incl_scan<unsigned>(c);
     unsigned long long total;
-    unsigned long long wex = block_excl_scan<unsigned long long>(lane == 0 ? cnt : 0u, sh, &total);
-    wex = __shfl_sync(0xffffffffu, wex, 0);
+    unsigned long long wex = block_excl_scan<unsigned long long>(lane == 31 ? incl : 0u, sh, &total);
+    wex = __shfl_sync(0xffffffffu, wex, 31);
     if (threadIdx.x < 32) {
       const unsigned long long ex_ = lookback_warp(status, tile, total);
       if (threadIdx.x == 0) base_sh = ex_;
     }
     __syncthreads();
-    unsigned long long r = base_sh + wex;
-    for (int k = 0; k < 32; k++) {
-      if (w0 + k * 32 >= nw) break;
-      const uint32_t m = __shfl_sync(0xffffffffu, my_mask, k);
-      if ((m >> lane) & 1) {
-        const unsigned long long i = w0 + k * 32 + lane;
-        const uint64_t v = src.word(i);
-        const unsigned long long dst = r + __popc(m & ((1u << lane) - 1));
-        uint8_t* p = payload + dst * width;
-        if (width == 1)
-          *p = (uint8_t)v;
-        else if (width == 2)
-          *reinterpret_cast<uint16_t*>(p) = (uint16_t)v;
-        else if (width == 4)
-          *reinterpret_cast<uint32_t*>(p) = (uint32_t)v;
-        else
-          *reinterpret_cast<uint64_t*>(p) = v;
+    unsigned long long dst = base_sh + wex + incl - c;
+    if (mask) {
+#pragma unroll
+      for (int j = 0; j < 32; j++) {
+        if ((mask >> (31 - j)) & 1) {
+          uint8_t* p = payload + dst * width;
+          if (width == 1)
+            *p = (uint8_t)v[j];
+          else if (width == 2)
+            *reinterpret_cast<uint16_t*>(p) = (uint16_t)v[j];
+          else if (width == 4)
+            *reinterpret_cast<uint32_t*>(p) = (uint32_t)v[j];
+          else
+            *reinterpret_cast<uint64_t*>(p) = v[j];
+          dst++;
+        }
       }
-      r += __popc(m);
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) lv->kept = base_sh + total;
     __syncthreads();
@@ -263,6 +318,28 @@ __global__ void __launch_bounds__(RD_THREADS)
     lv->active = 1;
   }
   reduce_tiles(src, nw, 2, 1, bitmap, payload, lb, lv);
+}
+
+// dst[0..n) = src[0..n) for a 4-byte aligned src and any dst: aligned 32-bit
+// stores built with funnel shifts from two aligned source words; the few
+// unaligned head bytes go byte-wise.  Grid-stride over (tid, nth).
+__device__ __forceinline__ void copy_to_unaligned(uint8_t* dst, const uint8_t* src, unsigned long long n,
+                                                  unsigned long long tid, unsigned long long nth) {
+  const unsigned head = (unsigned)((4 - ((uintptr_t)dst & 3)) & 3);
+  const unsigned long long h = head < n ? head : n;
+  for (unsigned long long i = tid; i < h; i += nth) dst[i] = src[i];
+  if (n <= h) return;
+  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + h);
+  const unsigned long long nw = (n - h) >> 2;
+  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);  // aligned
+  const int sh = (int)(h & 3) * 8;  // source byte offset of d32[0] is h
+  for (unsigned long long i = tid; i < nw; i += nth) {
+    const unsigned long long b = h + 4 * i;  // source byte index
+    const uint32_t lo = s32[b >> 2];
+    const uint32_t hi = sh ? s32[(b >> 2) + 1] : 0u;
+    d32[i] = sh ? __funnelshift_r(lo, hi, sh) : lo;
+  }
+  for (unsigned long long i = h + 4 * nw + tid; i < n; i += nth) dst[i] = src[i];
 }
 
 struct ChainLayout {
@@ -322,18 +399,10 @@ __global__ void k_chain_assemble(int stage, int width0, BmState* bm, uint8_t* co
   // copy ranges: raw bitmap of the last level, then payloads of levels 0..last
   const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned long long nth = (unsigned long long)gridDim.x * blockDim.x;
-  {
-    const uint8_t* src = bitmaps[L.last];
-    uint8_t* d = dst + L.off[L.last] + 19;
-    const unsigned long long n = bm->lv[L.last].bm_len;
-    for (unsigned long long i = tid; i < n; i += nth) d[i] = src[i];
-  }
+  copy_to_unaligned(dst + L.off[L.last] + 19, bitmaps[L.last], bm->lv[L.last].bm_len, tid, nth);
   for (int k = 0; k <= L.last; k++) {
     const int w = k == 0 ? width0 : 1;
-    const uint8_t* src = payloads[k];
-    uint8_t* d = dst + L.pay_off[k];
-    const unsigned long long n = bm->lv[k].kept * w;
-    for (unsigned long long i = tid; i < n; i += nth) d[i] = src[i];
+    copy_to_unaligned(dst + L.pay_off[k], payloads[k], bm->lv[k].kept * w, tid, nth);
   }
   // zero pad to the next 8-byte boundary (+8) for word-reading consumers
   const unsigned long long end = L.rec_len[0];
@@ -659,8 +728,7 @@ __global__ void k_archive_tail(uint8_t* arch, unsigned long long base, int prec,
   const unsigned long long slen = esc ? n : enc;
   const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned long long nth = (unsigned long long)gridDim.x * blockDim.x;
-  if (esc)
-    for (unsigned long long i = tid; i < n; i += nth) arch[soff + i] = seq[i];
+  if (esc) copy_to_unaligned(arch + soff, seq, n, tid, nth);
   if (tid == 0) {
     for (int i = 0; i < 46; i++) arch[i] = header46[i];
     arch[9] = esc ? 1 : 0;
@@ -766,51 +834,66 @@ __global__ void __launch_bounds__(RD_THREADS)
     const unsigned long long tile = tile_sh;
     if (tile >= ntiles) break;
     const unsigned long long w0 = tile * RD_TILE + (unsigned long long)wid * 1024;
-    // lane j fetches the bitmap word (32 symbols) of step j
-    uint32_t my_mask = 0;
-    {
-      const unsigned long long i0 = w0 + lane * 32;
-      if (i0 < nsym) {
-        const unsigned long long bb = i0 >> 3, nbm = cdiv(nsym, 8);
-        uint32_t be = 0;
-        for (int q = 0; q < 4; q++) be |= (bb + q < nbm ? (uint32_t)bm[bb + q] : 0u) << (24 - 8 * q);
-        const unsigned long long valid = nsym - i0;
-        if (valid < 32) be &= ~(0xFFFFFFFFu >> valid);
-        my_mask = be;  // bit (31 - l) = word i0 + l
-      }
+    // each lane owns 32 consecutive output words (one bitmap word)
+    const unsigned long long i0 = w0 + (unsigned long long)lane * 32;
+    uint32_t mask = 0;
+    if (i0 < nsym) {
+      const unsigned long long bb = i0 >> 3, nbm = cdiv(nsym, 8);
+      uint32_t be = 0;
+      for (int q = 0; q < 4; q++) be |= (bb + q < nbm ? (uint32_t)bm[bb + q] : 0u) << (24 - 8 * q);
+      const unsigned long long valid = nsym - i0;
+      if (valid < 32) be &= ~(0xFFFFFFFFu >> valid);
+      mask = be;  // bit (31 - j) = word i0 + j
     }
-    const unsigned cnt = warp_sum<unsigned>(__popc(my_mask));
+    const unsigned c = __popc(mask);
+    const unsigned incl = warp_incl_scan<unsigned>(c);
     unsigned long long total;
-    unsigned long long wex = block_excl_scan<unsigned long long>(lane == 0 ? cnt : 0u, sh, &total);
-    wex = __shfl_sync(0xffffffffu, wex, 0);
+    unsigned long long wex = block_excl_scan<unsigned long long>(lane == 31 ? incl : 0u, sh, &total);
+    wex = __shfl_sync(0xffffffffu, wex, 31);
     if (threadIdx.x < 32) {
       const unsigned long long ex_ = lookback_warp(lb + 1, tile, total);
       if (threadIdx.x == 0) base_sh = ex_;
     }
     __syncthreads();
-    unsigned long long r = base_sh + wex;  // ones before this warp's words
-    if (stg == 2 && tile == 0 && threadIdx.x == 0 && !(my_mask >> 31)) raise_flag(st, F_STAGE, 121);
-    for (int j = 0; j < 32; j++) {
-      if (w0 + j * 32 >= nsym) break;  // warp-uniform
-      const unsigned long long i = w0 + j * 32 + lane;
-      const uint32_t m = __shfl_sync(0xffffffffu, my_mask, j);
-      if (i < nsym) {
-        const int bit = (m >> (31 - lane)) & 1;
-        const unsigned long long before = r + (lane ? __popc(m >> (32 - lane)) : 0);
-        uint64_t v = 0;
+    if (stg == 2 && tile == 0 && threadIdx.x == 0 && !(mask >> 31)) raise_flag(st, F_STAGE, 121);
+    if (i0 < nsym) {
+      unsigned long long before = base_sh + wex + incl - c;  // ones before word i0
+      uint64_t v[32];
+#pragma unroll
+      for (int j = 0; j < 32; j++) {
+        const int bit = (mask >> (31 - j)) & 1;
+        uint64_t x = 0;
         if (stg == 2) {
           const unsigned long long idx = before + bit;  // inclusive count
-          if (idx >= 1 && idx <= npay) v = w == 1 ? pay[idx - 1] : ld_bytes(pay + (idx - 1) * w, w);
+          if (idx >= 1 && idx <= npay) x = w == 1 ? pay[idx - 1] : ld_bytes(pay + (idx - 1) * w, w);
         } else if (bit && before < npay) {
-          v = w == 1 ? pay[before] : ld_bytes(pay + before * w, w);
+          x = w == 1 ? pay[before] : ld_bytes(pay + before * w, w);
         }
-        uint8_t* p = out + i * w;
-        if (w == 1)
-          *p = (uint8_t)v;
-        else
-          st_bytes(p, v, w);
+        before += bit;
+        v[j] = x;
       }
-      r += __popc(m);
+      uint8_t* o = out + i0 * w;
+      if (w == 1) {
+        uint32_t u[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+          u[k] = (uint32_t)v[4 * k] | ((uint32_t)v[4 * k + 1] << 8) | ((uint32_t)v[4 * k + 2] << 16) |
+                 ((uint32_t)v[4 * k + 3] << 24);
+        uint4* q = reinterpret_cast<uint4*>(o);
+        q[0] = make_uint4(u[0], u[1], u[2], u[3]);
+        q[1] = make_uint4(u[4], u[5], u[6], u[7]);
+      } else if (w == 4) {
+        uint4* q = reinterpret_cast<uint4*>(o);
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+          q[k] = make_uint4((uint32_t)v[4 * k], (uint32_t)v[4 * k + 1], (uint32_t)v[4 * k + 2], (uint32_t)v[4 * k + 3]);
+      } else if (w == 8) {
+#pragma unroll
+        for (int k = 0; k < 32; k++) reinterpret_cast<uint64_t*>(o)[k] = v[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; k++) reinterpret_cast<uint16_t*>(o)[k] = (uint16_t)v[k];
+      }
     }
     if (tile == ntiles - 1 && threadIdx.x == 0 && base_sh + total != npay) raise_flag(st, F_STAGE, 122);
     __syncthreads();
