@@ -480,88 +480,113 @@ void launch_hist(const uint8_t* in, unsigned long long n, DevState* st, cudaStre
   (*launches)++;
 }
 
-__global__ void __launch_bounds__(256) k_huff_build(DevState* st, unsigned long long n, uint8_t* rec) {
+__global__ void __launch_bounds__(512) k_huff_build(DevState* st, unsigned long long n, uint8_t* rec) {
   __shared__ unsigned long long f[256];
   __shared__ int sorted[256];
   __shared__ int parent[512];
   __shared__ unsigned long long ifreq[256];
-  __shared__ int depth[512];
+  __shared__ int anc[512], dep[512];
   __shared__ uint8_t len[256];
-  __shared__ int np_sh;
+  __shared__ int np_sh, cnt[64];
+  __shared__ unsigned long long first[64];
   __shared__ unsigned long long red[33];
   const int t = threadIdx.x;
-  f[t] = st->hist[t];
+  if (t < 256) {
+    f[t] = st->hist[t];
+    len[t] = 0;
+  }
+  if (t < 64) cnt[t] = 0;
   if (t == 0) np_sh = 0;
   __syncthreads();
-  if (f[t]) atomicAdd(&np_sh, 1);
-  len[t] = 0;
+  if (t < 256 && f[t]) atomicAdd(&np_sh, 1);
   __syncthreads();
   const int np = np_sh;
-  if (f[t]) {  // rank by (freq, symbol)
+  if (t < 256 && f[t]) {  // rank by (freq, symbol) = heap pop order of the leaves
+    const unsigned long long ft = f[t];
     int r = 0;
-    for (int j = 0; j < 256; j++)
-      if (f[j] && (f[j] < f[t] || (f[j] == f[t] && j < t))) r++;
+    for (int j = 0; j < 256; j++) {
+      const unsigned long long fj = f[j];
+      r += fj && (fj < ft || (fj == ft && j < t));
+    }
     sorted[r] = t;
   }
   __syncthreads();
-  if (t == 0) {
-    if (np == 1) {
-      len[sorted[0]] = 1;
-    } else if (np > 1) {
-      int li = 0, ih = 0, it = 0;
-      for (int m = 0; m < np - 1; m++) {
-        int pick[2];
-        unsigned long long pf[2];
-        for (int q = 0; q < 2; q++) {
-          const bool la = li < np, ia = ih < it;
-          // leaf ids (< 256) precede internal ids on equal freq
-          if (la && (!ia || f[sorted[li]] <= ifreq[ih])) {
-            pick[q] = sorted[li];
-            pf[q] = f[sorted[li]];
-            li++;
-          } else {
-            pick[q] = 256 + ih;
-            pf[q] = ifreq[ih];
-            ih++;
-          }
-        }
-        parent[pick[0]] = 256 + m;
-        parent[pick[1]] = 256 + m;
-        ifreq[it++] = pf[0] + pf[1];
+  // heapq on (freq, id) == two-queue merge: leaves in (freq, sym) order,
+  // internal nodes FIFO (ids ascending, freqs non-decreasing), leaf first on ties
+  if (t == 0 && np > 1) {
+    int li = 0, ih = 0;
+    unsigned long long fl = f[sorted[0]];
+    for (int m = 0; m < np - 1; m++) {
+      int pick0, pick1;
+      unsigned long long p0, p1;
+      if (li < np && (ih >= m || fl <= ifreq[ih])) {
+        pick0 = sorted[li], p0 = fl;
+        li++;
+        fl = li < np ? f[sorted[li]] : 0;
+      } else {
+        pick0 = 256 + ih, p0 = ifreq[ih];
+        ih++;
       }
-      const int root = 256 + np - 2;
-      depth[root] = 0;
-      for (int node = root - 1; node >= 256; node--) depth[node] = depth[parent[node]] + 1;
-      for (int sym = 0; sym < 256; sym++)
-        if (f[sym]) len[sym] = (uint8_t)(depth[parent[sym]] + 1);
+      if (li < np && (ih >= m || fl <= ifreq[ih])) {
+        pick1 = sorted[li], p1 = fl;
+        li++;
+        fl = li < np ? f[sorted[li]] : 0;
+      } else {
+        pick1 = 256 + ih, p1 = ifreq[ih];
+        ih++;
+      }
+      parent[pick0] = 256 + m;
+      parent[pick1] = 256 + m;
+      ifreq[m] = p0 + p1;
     }
   }
   __syncthreads();
-  // canonical codes: rank by (len, sym)
-  __shared__ int csorted[256];
-  if (len[t]) {
-    int r = 0;
-    for (int j = 0; j < 256; j++)
-      if (len[j] && (len[j] < len[t] || (len[j] == len[t] && j < t))) r++;
-    csorted[r] = t;
+  // depths by pointer jumping over the parent links (root = 256 + np - 2)
+  if (np > 1) {
+    const int root = 256 + np - 2;
+    const bool node = (t < 256 && f[t]) || (t >= 256 && t <= root);
+    anc[t] = node && t != root ? parent[t] : t;
+    dep[t] = node && t != root ? 1 : 0;
+    __syncthreads();
+    for (int k = 0; k < 9; k++) {
+      const int a = anc[t];
+      const int d = dep[t] + dep[a];
+      const int aa = anc[a];
+      __syncthreads();
+      dep[t] = d;
+      anc[t] = aa;
+      __syncthreads();
+    }
+    if (t < 256 && f[t]) len[t] = (uint8_t)dep[t];
+  } else if (np == 1 && t == 0) {
+    len[sorted[0]] = 1;
   }
   __syncthreads();
-  if (t == 0) {
-    unsigned long long next = 0;
-    int prev = 0;
-    for (int i = 0; i < np; i++) {
-      const int sym = csorted[i];
-      const int L = len[sym];
-      const int sh = L - prev;
-      next = sh >= 64 ? 0 : next << sh;
-      st->hf_code[sym] = next++;
-      prev = L;
+  // canonical codes (stages.py:275-287): per length the first code, then rank
+  if (t < 256 && len[t]) atomicAdd(&cnt[len[t]], 1);
+  __syncthreads();
+  if (t == 0) {  // first code per length: start[L+1] = (start[L] + count[L]) << 1
+    unsigned long long c = 0;
+    for (int L = 1; L < 64; L++) {
+      first[L] = c;
+      c = (c + cnt[L]) << 1;
     }
   }
-  st->hf_len[t] = len[t];
+  __syncthreads();
+  if (t < 256) {
+    const int L = len[t];
+    unsigned long long c = 0;
+    if (L) {
+      int r = 0;
+      for (int j = 0; j < t; j++) r += len[j] == L;
+      c = first[L] + r;
+    }
+    st->hf_code[t] = c;
+    st->hf_len[t] = (uint8_t)L;
+  }
   // nbits = sum hist * len
   unsigned long long tot;
-  block_excl_scan<unsigned long long>(f[t] * len[t], red, &tot);
+  block_excl_scan<unsigned long long>(t < 256 ? f[t] * len[t] : 0ull, red, &tot);
   if (t == 0) {
     const unsigned long long nbits = n ? tot : 0;
     st->hf_nbits = nbits;
@@ -573,11 +598,11 @@ __global__ void __launch_bounds__(256) k_huff_build(DevState* st, unsigned long 
     rec[274] = 0;
     rec[275] = 0;
   }
-  rec[18 + t] = len[t];
+  if (t < 256) rec[18 + t] = len[t];
 }
 
 void launch_huffman_build(DevState* st, unsigned long long n, uint8_t* hf_rec, cudaStream_t s, int* launches) {
-  k_huff_build<<<1, 256, 0, s>>>(st, n, hf_rec);
+  k_huff_build<<<1, 512, 0, s>>>(st, n, hf_rec);
   (*launches)++;
 }
 

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(TUNE_THREADS)
   __syncthreads();
   const uint8_t cb = c_choice[ci];
   const bool linear = cb & 1, seq1d = (cb >> 1) & 1;
-  const double eb = st->eb, two_eb = st->two_eb;
+  const double eb = st->eb, two_eb = st->two_eb, inv_two_eb = __ddiv_rn(1.0, two_eb);
   const int dims[3] = {b0, b1, b2};
   SubStep ss[7];
   const int nss = block_steps(dims, level, seq1d, ss);
@@ -190,13 +190,44 @@ __global__ void __launch_bounds__(TUNE_THREADS)
       const double o = (double)orig[lin];
       diff[idx] = fabs(__dsub_rn(o, pred));
       double r;
-      quantize<sizeof(T) == 4>(o, pred, eb, two_eb, &r);
+      quantize_fast<sizeof(T) == 4>(o, pred, eb, two_eb, inv_two_eb, &r);
       g[lin] = r;
     }
     __syncthreads();
     if (threadIdx.x == 0) nleaf = pw_leaves(n, lstart, llen);
     __syncthreads();
-    for (int i = threadIdx.x; i < nleaf; i += blockDim.x) leaf[i] = pw_leaf(diff + lstart[i], llen[i]);
+    // each leaf on 8 lanes: lane j owns numpy's accumulator r[j] (column j)
+    for (int base = 0; base < nleaf; base += TUNE_THREADS / 8) {
+      const int li = base + (int)(threadIdx.x >> 3), j = threadIdx.x & 7;
+      double r = 0.0;
+      int ln = 0;
+      const double* a = diff;
+      if (li < nleaf) {
+        ln = llen[li];
+        a = diff + lstart[li];
+        if (ln >= 8) {
+          r = a[j];
+          for (int i = 8; i < ln - (ln % 8); i += 8) r = __dadd_rn(r, a[i + j]);
+        }
+      }
+      const unsigned gmask = 0xFFu << (threadIdx.x & 24);
+      double rr[8];
+#pragma unroll
+      for (int q = 0; q < 8; q++) rr[q] = __shfl_sync(0xffffffffu, r, (threadIdx.x & 24) + q);
+      (void)gmask;
+      if (li < nleaf && j == 0) {
+        double res;
+        if (ln < 8) {
+          res = 0.0;
+          for (int i = 0; i < ln; i++) res = __dadd_rn(res, a[i]);
+        } else {
+          res = __dadd_rn(__dadd_rn(__dadd_rn(rr[0], rr[1]), __dadd_rn(rr[2], rr[3])),
+                          __dadd_rn(__dadd_rn(rr[4], rr[5]), __dadd_rn(rr[6], rr[7])));
+          for (int i = ln - (ln % 8); i < ln; i++) res = __dadd_rn(res, a[i]);
+        }
+        leaf[li] = res;
+      }
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
       int cur = 0;
