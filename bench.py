@@ -202,7 +202,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2507_11165_b200 as hb
-    from paper_2507_11165_b200 import _lib, synth
+    from paper_2507_11165_b200 import _lib, slabs, synth
+    from paper_2507_11165_b200.field import min_max as field_min_max
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -244,7 +245,17 @@ def run_ours(args):
     with Clocks(local) as clk:
         for k in range(args.steps):
             ev[k][0].record(stream)
-            a = hb.compress_device(f, spec, args.mode, out=out_buf)
+            if world > 1:
+                # slabs of one volume share the global rel-eb: device min/max
+                # (k_minmax), 2-float all-reduce, then an abs-eb compress
+                lo, hi = field_min_max(f)
+                mm = torch.tensor([float(hi), -float(lo)], dtype=torch.float64, device="cuda")
+                dist.all_reduce(mm, op=dist.ReduceOp.MAX)
+                launches += _lib.last_launch_count()
+                eb = slabs.global_abs_eb(spec, np.float32(-mm[1].item()), np.float32(mm[0].item()), np.float32)
+                a = hb.compress_device(f, hb.ErrorBoundSpec("abs", eb), args.mode, out=out_buf)
+            else:
+                a = hb.compress_device(f, spec, args.mode, out=out_buf)
             launches += _lib.last_launch_count()
             for nm, ms in _lib.last_phases():
                 phases.setdefault(nm, []).append(ms)

@@ -90,6 +90,10 @@ HB_API int hb_compress(hb_ctx* ctx, const void* field, int precision, const uint
                 double eb, int mode, void* out, size_t cap, size_t* out_len, double* abs_eb_out,
                 uint8_t cfg_out[4]);
 
+/* field.py:129-132 value_range on the device: min and max of n values (the
+ * reference subtracts them in the field dtype); FieldError on NaN/Inf. */
+HB_API int hb_value_range(hb_ctx* ctx, const void* field, int precision, uint64_t n, double* vmin, double* vmax);
+
 /* archive.py:93-118 on host bytes (no device work). */
 HB_API int hb_archive_info(const void* host_blob, size_t len, hb_info* info);
 

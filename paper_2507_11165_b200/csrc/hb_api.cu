@@ -465,6 +465,44 @@ int hb_compress_bound(const uint64_t dims[3], int precision, size_t* max_bytes) 
   return HB_OK;
 }
 
+int hb_value_range(hb_ctx* ctx, const void* field, int prec, uint64_t n, double* vmin, double* vmax) {
+  if (!ctx || !field || !vmin || !vmax || n == 0) return ctx ? set_err(ctx, HB_EARG, "bad argument") : HB_EARG;
+  if (prec != 4 && prec != 8) return set_err(ctx, HB_EFIELD, "unsupported precision %d", prec);
+  cudaSetDevice(ctx->device);
+  const cudaStream_t s = ctx->stream;
+  Layout L;
+  const size_t o_st = L.take(sizeof(DevState));
+  const bool host = mem_kind(field) == MEM_HOST;
+  const size_t o_f = host ? L.take(n * prec + 64) : 0;
+  int rc = ensure_arena(ctx, L.off);
+  if (rc) return rc;
+  DevState* st = reinterpret_cast<DevState*>(ctx->arena + o_st);
+  const void* f = field;
+  if (host) {
+    CU(cudaMemcpyAsync(ctx->arena + o_f, field, n * prec, cudaMemcpyHostToDevice, s));
+    f = ctx->arena + o_f;
+  }
+  int nl = 0;
+  CU(cudaMemsetAsync(st, 0, sizeof(DevState), s));
+  launch_minmax(f, prec, n, st, 1, 1.0, s, &nl);
+  ctx->launches = nl;
+  unsigned long long* h = reinterpret_cast<unsigned long long*>(ctx->pinned + 4096);
+  CU(cudaMemcpyAsync(h, &st->vmin_bits, 16, cudaMemcpyDeviceToHost, s));
+  HostStatus hs;
+  rc = read_status(ctx, st, &hs);
+  if (rc) return rc;
+  if (hs.flags & F_NONFINITE) return set_err(ctx, HB_EFIELD, "field contains NaN or Inf values");
+  auto dec = [](unsigned long long o) {
+    unsigned long long b = (o >> 63) ? (o & ~(1ull << 63)) : ~o;
+    double d;
+    memcpy(&d, &b, 8);
+    return d;
+  };
+  *vmin = dec(h[0]);
+  *vmax = dec(h[1]);
+  return HB_OK;
+}
+
 int hb_archive_info(const void* host_blob, size_t len, hb_info* info) {
   if (!host_blob || !info) return HB_EARG;
   return parse_info((const uint8_t*)host_blob, len, info, nullptr);

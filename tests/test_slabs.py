@@ -1,0 +1,110 @@
+"""Slab container and the distributed slab driver.
+
+CPU tests: the per-slab compressor is injected (the oracle, test-only) so the
+host logic -- bounds, global eb all-reduce, size all-gather, offsets,
+container layout -- runs on gloo with world_size 2.  The GPU test runs the
+real CUDA compressor.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import has_cuda
+
+import paper_2507_11165_b200 as hb
+from paper_2507_11165_b200 import slabs, synth
+
+
+def oracle_compress(f, spec, mode):
+    from oracle import oracle
+    return oracle.compress(np.ascontiguousarray(f.values), spec.mode, spec.magnitude, mode, f.ndim)
+
+
+def oracle_decompress(blob):
+    from oracle import oracle
+    out, _ = oracle.decompress(blob)
+    return out
+
+
+def test_slab_bounds():
+    assert slabs.slab_bounds(10, 3) == [(0, 4), (4, 7), (7, 10)]
+    assert slabs.slab_bounds(8, 8)[-1] == (7, 8)
+    with pytest.raises(ValueError):
+        slabs.slab_bounds(4, 5)
+
+
+def test_container_round_trip_single_process(oracle):
+    vals = synth.make("grf", (48, 40, 36), seed=3)
+    f = hb.Field(vals)
+    spec = hb.ErrorBoundSpec("rel", 1e-3)
+    blob = slabs.compress_slabs(f, spec, "cr", 3, compress_fn=oracle_compress)
+    dims, ndim, prec, mode, ents = slabs.parse(blob)
+    assert dims == (48, 40, 36) and ndim == 3 and prec == 4 and mode == "cr" and len(ents) == 3
+    eb = oracle.resolve_eb(vals, "rel", 1e-3)
+    for (x0, x1, o, n) in ents:  # every slab is a plain reference-format archive
+        ref = oracle.compress(np.ascontiguousarray(vals[x0:x1]), "abs", eb, "cr", 3)
+        assert blob[o:o + n] == ref
+    out = slabs.decompress_slabs(blob, decompress_fn=oracle_decompress)
+    assert np.max(np.abs(out.values.astype(np.float64) - vals)) <= eb
+    with pytest.raises(hb.ArchiveError):
+        slabs.parse(blob[:20])
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, vals, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    bounds = slabs.slab_bounds(vals.shape[0], world)
+    x0, x1 = bounds[rank]
+    spec = hb.ErrorBoundSpec("rel", 1e-3)
+    arc, off, head = slabs.compress_distributed(np.ascontiguousarray(vals[x0:x1]), x0, vals.shape, spec, "tp",
+                                                compress_fn=oracle_compress)
+    full = slabs.gather_container(arc, x0, head)
+    q.put((rank, off, len(arc), full))
+    dist.destroy_process_group()
+
+
+def test_distributed_gloo_world2(oracle):
+    import multiprocessing as mp
+    vals = synth.make("rough", (40, 33, 30), seed=5)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, vals, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in ps:
+        p.join(timeout=60)
+    res.sort()
+    full = res[0][3]
+    assert full is not None and res[1][3] is None
+    single = slabs.compress_slabs(hb.Field(vals), hb.ErrorBoundSpec("rel", 1e-3), "tp", 2,
+                                  compress_fn=oracle_compress)
+    assert full == single  # same bytes as the single-process container
+    dims, ndim, prec, mode, ents = slabs.parse(full)
+    assert [(o, n) for _, _, o, n in ents] == [(res[0][1], res[0][2]), (res[1][1], res[1][2])]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_gpu_slab_container_matches_oracle(oracle):
+    vals = synth.make("grf", (64, 48, 40), seed=9)
+    f = hb.Field(vals)
+    spec = hb.ErrorBoundSpec("rel", 1e-3)
+    gpu = slabs.compress_slabs(f, spec, "cr", 4)
+    ref = slabs.compress_slabs(f, spec, "cr", 4, compress_fn=oracle_compress)
+    assert gpu == ref
+    out = slabs.decompress_slabs(gpu)
+    assert np.max(np.abs(out.values.astype(np.float64) - vals)) <= oracle.resolve_eb(vals, "rel", 1e-3)
