@@ -531,9 +531,7 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
   tp.bn = (unsigned long long)tp.shape[0] * tp.shape[1] * tp.shape[2];
   tp.top = ilog2i(anchor_stride(std::vector<uint64_t>{(uint64_t)tp.shape[0], (uint64_t)tp.shape[1],
                                                       (uint64_t)tp.shape[2]}.data()));
-  if (tp.top > 0 && !tune_supported(tp))
-    return set_err(ctx, HB_EUNSUPPORTED, "thin field: whole-field tuner block of %llu points is too large",
-                   (unsigned long long)tp.bn);
+  const bool tune_global = tp.top > 0 && !tune_supported(tp);  // thin field: whole-field block in HBM
   size_t bound;
   hb_compress_bound(dims, prec, &bound);
   // ---- layout
@@ -547,7 +545,7 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
   const size_t o_seq = L.take(N + 128);
   const size_t o_obm = L.take(cdiv(N, 32) * 4 + 64);
   const size_t o_org = L.take(org.size() * 8 + 8);
-  const size_t o_trials = L.take((size_t)2 * 4 * tp.nb * tp.bn * 8);
+  const size_t o_trials = L.take(tune_global ? tune_global_bytes(tp.bn) : (size_t)2 * 4 * tp.nb * tp.bn * 8);
   const size_t o_berr = L.take((size_t)4 * tp.nb * 8);
   const size_t o_arch = L.take(bound + N / 4 + 4096);
   const unsigned long long hf_max = 274 + N + 64;
@@ -572,7 +570,7 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
   const size_t lb_bytes = (lb_oc + lb_he + 4 * lb_c1 + 4 * lb_c2) * 8;
   rc = ensure_arena(ctx, L.off);
   if (rc) return rc;
-  rc = ensure_pinned(ctx, 8192 + org.size() * 8 + 4096);
+  rc = ensure_pinned(ctx, 8192 + 4096 + org.size() * 8 + (tune_global ? (tp.bn / 32 + 64) * 8 + 4096 : 0));
   if (rc) return rc;
   uint8_t* base = ctx->arena;
   DevState* st = reinterpret_cast<DevState*>(base + o_st);
@@ -609,9 +607,20 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
   launch_minmax(dfield, prec, N, st, eb_mode, mag, s, &nl);
   ctx->mark("eb_range");
   // 2) tuner (tuning.py:105-150)
-  for (int level = tp.top; level >= 1; level--) {
-    launch_tune_level(tp, dfield, prec, dims, d_org, level, trials, berr, st, s, &nl);
-    launch_tune_select(tp, level, berr, st, s, &nl);
+  if (tune_global) {
+    auto upfn = [](void* c, void* dev, const void* src, size_t n) -> int {
+      PinnedUp* u = reinterpret_cast<PinnedUp*>(c);
+      u->off = 8192 + 4096;  // scratch region reused per sub-step (the tuner syncs after each)
+      return u->put(dev, src, n, u->ctx->stream);
+    };
+    PinnedUp tup{ctx};
+    rc = launch_tune_global(dfield, prec, dims, tp.top, reinterpret_cast<uint8_t*>(trials), st, s, &nl, upfn, &tup);
+    if (rc) return rc;
+  } else {
+    for (int level = tp.top; level >= 1; level--) {
+      launch_tune_level(tp, dfield, prec, dims, d_org, level, trials, berr, st, s, &nl);
+      launch_tune_select(tp, level, berr, st, s, &nl);
+    }
   }
   ctx->mark("tune");
   if (!tune_only) {

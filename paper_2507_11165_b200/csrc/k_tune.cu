@@ -11,6 +11,9 @@
 // winner whose trial grids seed the next level (:140).
 #include <cuda_runtime.h>
 
+#include <utility>
+#include <vector>
+
 #include "hb_common.cuh"
 #include "hb_interp.cuh"
 #include "hb_kernels.h"
@@ -297,6 +300,216 @@ void launch_tune_select(const TunePlan& p, int level, const double* berr, DevSta
                         int* launches) {
   k_tune_select<<<1, 32, 0, s>>>(p.nb, level, berr, st);
   (*launches)++;
+}
+
+// ------------------------------------------------ whole-field (thin) tuner
+// plan_blocks returns the whole field as the single sample block when its
+// smallest non-degenerate dim is < 17 (tuning.py:74-75).  Blocks too large for
+// shared memory run here on global-memory grids: one launch per sub-step, the
+// |orig - pred| array of each sub-step materialised in C order, numpy's
+// pairwise sum over it (parallel leaves, recursive combine), and the same
+// argmin / winner hand-over as the tiled path (nb = 1, so Python's sum over
+// blocks is the single total).
+
+struct HSub {  // host copy of one sub-step
+  int start[3], step[3], count[3];
+  int axes[3];
+  int k;
+};
+
+static int host_steps(const int d[3], int level, bool seq1d, HSub* out) {
+  const int s = 1 << (level - 1);
+  int n = 0;
+  if (seq1d) {
+    int o[3] = {0, 1, 2};
+    for (int i = 0; i < 3; i++)
+      for (int j = i + 1; j < 3; j++)
+        if (d[o[j]] > d[o[i]] || (d[o[j]] == d[o[i]] && o[j] < o[i])) std::swap(o[i], o[j]);
+    for (int k = 0; k < 3; k++) {
+      const int a = o[k];
+      HSub ss;
+      for (int j = 0; j < 3; j++) {
+        bool earlier = false;
+        for (int m = 0; m < k; m++) earlier |= o[m] == j;
+        ss.start[j] = j == a ? s : 0;
+        ss.step[j] = j == a ? 2 * s : (earlier ? s : 2 * s);
+        ss.count[j] = d[j] > ss.start[j] ? (d[j] - ss.start[j] + ss.step[j] - 1) / ss.step[j] : 0;
+      }
+      ss.axes[0] = a;
+      ss.k = 1;
+      if (ss.count[a] > 0) out[n++] = ss;
+    }
+  } else {
+    const int sets[7] = {1, 2, 4, 3, 5, 6, 7};
+    for (int t = 0; t < 7; t++) {
+      HSub ss;
+      bool empty = false;
+      ss.k = 0;
+      for (int j = 0; j < 3; j++) {
+        const bool odd = (sets[t] >> j) & 1;
+        ss.start[j] = odd ? s : 0;
+        ss.step[j] = 2 * s;
+        ss.count[j] = d[j] > ss.start[j] ? (d[j] - ss.start[j] + ss.step[j] - 1) / ss.step[j] : 0;
+        if (odd) {
+          if (ss.count[j] == 0) empty = true;
+          ss.axes[ss.k++] = j;
+        }
+      }
+      if (!empty) out[n++] = ss;
+    }
+  }
+  return n;
+}
+
+template <typename T>
+__global__ void k_tg_init(const T* __restrict__ f, unsigned long long n, double* g) {
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    g[i] = (double)f[i];
+}
+
+__global__ void k_tg_copy(const double* __restrict__ src_base, unsigned long long stride, const DevState* st,
+                          int level, unsigned long long n, double* dst) {
+  const double* src = src_base + (size_t)st->tune_winner[level - 1] * stride;  // winner of `level`
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+template <typename T>
+__global__ void k_tg_step(const T* __restrict__ f, HSub S, int d0, int d1, int d2, int level, int linear,
+                          double* g, double* diff, DevState* st) {
+  const unsigned long long n = (unsigned long long)S.count[0] * S.count[1] * S.count[2];
+  const int s = 1 << (level - 1);
+  const int dims[3] = {d0, d1, d2};
+  const double eb = st->eb, two_eb = st->two_eb, inv_two_eb = __ddiv_rn(1.0, two_eb);
+  for (unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (unsigned long long)gridDim.x * blockDim.x) {
+    long long c[3];
+    c[2] = S.start[2] + (long long)(idx % S.count[2]) * S.step[2];
+    c[1] = S.start[1] + (long long)((idx / S.count[2]) % S.count[1]) * S.step[1];
+    c[0] = S.start[0] + (long long)(idx / ((unsigned long long)S.count[2] * S.count[1])) * S.step[0];
+    const long long lin = (c[0] * d1 + c[1]) * d2 + c[2];
+    double pv[3];
+    int ov[3];
+    for (int i = 0; i < S.k; i++) {
+      const int a = S.axes[i];
+      const long long stp = (a == 0 ? (long long)d1 * d2 : (a == 1 ? (long long)d2 : 1ll)) * s;
+      const int cls = classify(c[a], dims[a], s, linear);
+      const double v0 = c[a] >= 3 * s ? g[lin - 3 * stp] : 0.0;
+      const double v1 = g[lin - stp];
+      const double v2 = c[a] + s < dims[a] ? g[lin + stp] : 0.0;
+      const double v3 = c[a] + 3 * s < dims[a] ? g[lin + 3 * stp] : 0.0;
+      pv[i] = apply_stencil(cls, v0, v1, v2, v3);
+      ov[i] = stencil_order(cls);
+    }
+    const double pred = S.k == 1 ? pv[0] : combine_axes(S.k, pv, ov);
+    const double o = (double)f[lin];
+    diff[idx] = fabs(__dsub_rn(o, pred));
+    double r;
+    quantize_fast<sizeof(T) == 4>(o, pred, eb, two_eb, inv_two_eb, &r);
+    g[lin] = r;
+  }
+}
+
+__global__ void k_tg_leaves(const double* __restrict__ diff, const int2* __restrict__ leaves, int nleaf,
+                            double* leafsum) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nleaf; i += gridDim.x * blockDim.x)
+    leafsum[i] = pw_leaf(diff + leaves[i].x, leaves[i].y);
+}
+
+// total += pairwise(n) from the leaf sums (recursion of numpy's pairwise_sum)
+__device__ double tg_combine(unsigned long long n, const double* leaf, unsigned long long* cur) {
+  if (n <= 128) return leaf[(*cur)++];
+  unsigned long long n2 = n / 2;
+  n2 -= n2 % 8;
+  const double a = tg_combine(n2, leaf, cur);
+  const double b = tg_combine(n - n2, leaf, cur);
+  return __dadd_rn(a, b);
+}
+
+__global__ void k_tg_accum(unsigned long long n, const double* leafsum, double* total) {
+  unsigned long long cur = 0;
+  *total = __dadd_rn(*total, tg_combine(n, leafsum, &cur));
+}
+
+// tuning.py:135-140 for a single block: errs[c] = 0 + total[c]
+__global__ void k_tg_select(int level, double* totals, DevState* st) {
+  int best = 0;
+  for (int i = 0; i < 4; i++) {
+    const double e = __dadd_rn(0.0, totals[i]);
+    st->tune_errs[(level - 1) * 4 + i] = e;
+    if (i > 0 && e < __dadd_rn(0.0, totals[best])) best = i;
+  }
+  st->tune_winner[level - 1] = best;
+  st->cfg[level - 1] = c_choice[best];
+  for (int i = 0; i < 4; i++) totals[i] = 0.0;
+}
+
+size_t tune_global_bytes(unsigned long long bn) { return bn * 8 * 6 + 4096 * 16 + (bn / 32 + 64) * 16; }
+
+// scratch: [state | 4 trials | diff | leaf sums | totals]
+int launch_tune_global(const void* field, int prec, const uint64_t dims[3], int top, uint8_t* scratch,
+                       DevState* st, cudaStream_t s, int* launches,
+                       int (*upload)(void* ctx, void* dev, const void* src, size_t n), void* up_ctx) {
+  const unsigned long long bn = dims[0] * dims[1] * dims[2];
+  double* state = reinterpret_cast<double*>(scratch);
+  double* trial = state + bn;
+  double* diff = trial + 4 * bn;
+  double* leafsum = diff + bn;
+  double* totals = leafsum + (bn / 32 + 64);
+  int2* leaves = reinterpret_cast<int2*>(totals + 8);
+  const int d[3] = {(int)dims[0], (int)dims[1], (int)dims[2]};
+  const unsigned grid = 148 * 8;
+  if (prec == 4)
+    k_tg_init<float><<<grid, 256, 0, s>>>((const float*)field, bn, state);
+  else
+    k_tg_init<double><<<grid, 256, 0, s>>>((const double*)field, bn, state);
+  (*launches)++;
+  cudaMemsetAsync(totals, 0, 8 * sizeof(double), s);
+  for (int level = top; level >= 1; level--) {
+    for (int ci = 0; ci < 4; ci++) {
+      const uint8_t cb = ci == 0 ? 0 : (ci == 1 ? 2 : (ci == 2 ? 1 : 3));
+      double* g = trial + (size_t)ci * bn;
+      cudaMemcpyAsync(g, state, bn * 8, cudaMemcpyDeviceToDevice, s);
+      HSub ss[7];
+      const int nss = host_steps(d, level, (cb >> 1) & 1, ss);
+      for (int t = 0; t < nss; t++) {
+        const unsigned long long n = (unsigned long long)ss[t].count[0] * ss[t].count[1] * ss[t].count[2];
+        if (prec == 4)
+          k_tg_step<float><<<grid, 256, 0, s>>>((const float*)field, ss[t], d[0], d[1], d[2], level, cb & 1, g,
+                                                diff, st);
+        else
+          k_tg_step<double><<<grid, 256, 0, s>>>((const double*)field, ss[t], d[0], d[1], d[2], level, cb & 1, g,
+                                                 diff, st);
+        // leaves of the recursion in order (host, depends on n only)
+        std::vector<int2> lv;
+        std::vector<std::pair<unsigned long long, unsigned long long>> stk{{0ull, n}};
+        while (!stk.empty()) {
+          auto [s0, n0] = stk.back();
+          stk.pop_back();
+          if (n0 <= 128) {
+            lv.push_back(make_int2((int)s0, (int)n0));
+          } else {
+            unsigned long long n2 = n0 / 2;
+            n2 -= n2 % 8;
+            stk.push_back({s0 + n2, n0 - n2});
+            stk.push_back({s0, n2});
+          }
+        }
+        const int rc = upload(up_ctx, leaves, lv.data(), lv.size() * sizeof(int2));
+        if (rc) return rc;
+        k_tg_leaves<<<(unsigned)((lv.size() + 255) / 256), 256, 0, s>>>(diff, leaves, (int)lv.size(), leafsum);
+        k_tg_accum<<<1, 1, 0, s>>>(n, leafsum, totals + ci);
+        *launches += 3;
+        cudaStreamSynchronize(s);  // the leaf table in pinned memory is reused by the next sub-step
+      }
+    }
+    k_tg_select<<<1, 1, 0, s>>>(level, totals, st);
+    k_tg_copy<<<grid, 256, 0, s>>>(trial, bn, st, level, bn, state);
+    *launches += 2;
+  }
+  return 0;
 }
 
 }  // namespace hb

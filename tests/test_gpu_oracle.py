@@ -57,3 +57,19 @@ def test_512_cubed_properties():
     assert torch.equal(r_cr.values, r_tp.values)  # CR/TP reconstructions identical
     err = (r_cr.values.double() - vals.double()).abs().max().item()
     assert err <= info["abs_eb"]
+
+
+@pytest.mark.parametrize("dims", [(12, 70, 65), (16, 48, 40), (9, 33, 200), (5, 300, 310)])
+def test_thin_field_whole_block_tuner(oracle, dims):
+    """min dim < 17: the tuner's single block is the whole field (tuning.py:74-75)."""
+    vals = synth.make("grf", dims, seed=4)
+    f = hb.Field(vals)
+    eb = oracle.resolve_eb(vals, "rel", 1e-3)
+    cfg, errs = oracle.tune(vals, eb)
+    rep = hb.tune_report(f, eb)
+    assert rep.chosen.to_bytes() == bytes(cfg)
+    for level, e in rep.level_errors.items():
+        for i, c in enumerate(hb.tuning.CONFIG_CHOICES):
+            assert e[c] == errs[level - 1, i]
+    for mode in ("cr", "tp"):
+        assert hb.compress(f, hb.ErrorBoundSpec("rel", 1e-3), mode) == oracle.compress(vals, "rel", 1e-3, mode, 3)
