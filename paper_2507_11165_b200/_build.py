@@ -43,6 +43,23 @@ def headers():
     return hs
 
 
+def local_deps(src, seen=None):
+    """src plus the csrc/include headers it #includes (transitively)."""
+    import re
+    seen = set() if seen is None else seen
+    if src in seen:
+        return seen
+    seen.add(src)
+    with open(src) as f:
+        for m in re.finditer(r'^\s*#include\s+"([^"]+)"', f.read(), re.M):
+            for d in (os.path.dirname(src), CSRC, os.path.join(ROOT, "include")):
+                c = os.path.join(d, m.group(1))
+                if os.path.exists(c):
+                    local_deps(c, seen)
+                    break
+    return seen
+
+
 def up_to_date() -> bool:
     if not os.path.exists(LIB):
         return False
@@ -55,11 +72,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     nv = nvcc()
-    hdr_t = max(os.path.getmtime(h) for h in headers())
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
-        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_t):
+        dep_t = max(os.path.getmtime(d) for d in local_deps(src))
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > dep_t:
             return obj
         cmd = [nv, *NVCC_FLAGS, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -623,6 +623,15 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
     }
   }
   ctx->mark("tune");
+  // the interpolation config picks the level-kernel instantiation: one small
+  // read-back after the tuner (the only mid-call synchronisation)
+  uint8_t hcfg[4] = {0, 0, 0, 0};
+  if (!tune_only && top > 0) {
+    uint8_t* pc = ctx->pinned + 4096 + 512;
+    CU(cudaMemcpyAsync(pc, st->cfg, 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    memcpy(hcfg, pc, 4);
+  }
   if (!tune_only) {
     // 3) anchors + the level walk with fused quantize / reorder / histogram
     const unsigned long long abase = 46 + 8;
@@ -631,7 +640,7 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
     for (int level = top; level >= 1; level--) {
       LevelGeom g;
       make_level_geom(dims, level, &g);
-      launch_level_compress(g, dfield, prec, E, seq, obm, st, s, &nl);
+      launch_level_compress(g, dfield, prec, E, seq, obm, st, s, &nl, hcfg[level - 1] & 3);
       ctx->mark(lvl_names[level]);
     }
     // 4) outliers straight into the archive (archive.py:65-71)
@@ -847,7 +856,7 @@ int hb_decompress(hb_ctx* ctx, const void* archive, size_t len, void* field_out,
     for (int level = top; level >= 1; level--) {
       LevelGeom g;
       make_level_geom(I.dims, level, &g);
-      launch_level_decompress(g, codes, oidx, oval, &st->scratch[3], E, out, prec, st, s, &nl);
+      launch_level_decompress(g, codes, oidx, oval, &st->scratch[3], E, out, prec, st, s, &nl, I.cfg[level - 1] & 3);
       static const char* dl_names[5] = {"", "rlevel1", "rlevel2", "rlevel3", "rlevel4"};
       ctx->mark(dl_names[level]);
     }
@@ -917,7 +926,8 @@ int hb_decompose(hb_ctx* ctx, const void* field, int prec, const uint64_t dims[3
   for (int level = top; level >= 1; level--) {
     LevelGeom g;
     make_level_geom(dims, level, &g);
-    launch_level_compress(g, dfield, prec, E, seq, reinterpret_cast<uint32_t*>(base + o_obm), st, s, &nl);
+    launch_level_compress(g, dfield, prec, E, seq, reinterpret_cast<uint32_t*>(base + o_obm), st, s, &nl,
+                          cfg[level - 1] & 3);
   }
   launch_outlier_compact(reinterpret_cast<uint32_t*>(base + o_obm), N, dfield, prec, nullptr,
                          reinterpret_cast<uint64_t*>(base + o_oidx), base + o_oval,
@@ -1001,7 +1011,7 @@ int hb_reconstruct(hb_ctx* ctx, const uint8_t* seq_in, const uint64_t* oidx_in, 
       make_level_geom(dims, level, &g);
       launch_level_decompress(g, base + o_seq, reinterpret_cast<uint64_t*>(base + o_oidx),
                               reinterpret_cast<double*>(base + o_oval), &st->scratch[3],
-                              reinterpret_cast<double*>(base + o_E), out, prec, st, s, &nl);
+                              reinterpret_cast<double*>(base + o_E), out, prec, st, s, &nl, cfg[level - 1] & 3);
     }
   }
   ctx->launches = nl;

@@ -46,7 +46,7 @@ void launch_anchor_init(const void* field, int prec, const uint64_t dims[3], int
                         uint8_t* anchors_out /*byte-addressed, may be unaligned*/, DevState* st, bool count_hist,
                         cudaStream_t s, int* launches);
 void launch_level_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq,
-                           uint32_t* obitmap, DevState* st, cudaStream_t s, int* launches);
+                           uint32_t* obitmap, DevState* st, cudaStream_t s, int* launches, int cfg = -1);
 void launch_outlier_compact(const uint32_t* obitmap, unsigned long long n, const void* field, int prec,
                             uint8_t* rec_out /*byte addressed*/, uint64_t* oidx_out, void* oval_out,
                             unsigned long long* lb_status, DevState* st, cudaStream_t s, int* launches);
@@ -54,7 +54,7 @@ void launch_anchor_load(const uint8_t* anchors /*byte addressed*/, int prec, con
                         double* E, cudaStream_t s, int* launches);
 void launch_level_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
                              const unsigned long long* ocount_dev, double* E, void* out, int prec, DevState* st,
-                             cudaStream_t s, int* launches);
+                             cudaStream_t s, int* launches, int cfg = -1);
 void launch_copy_anchors_out(const uint8_t* anchors, int prec, unsigned long long n, void* out, DevState* st,
                              cudaStream_t s, int* launches);
 void launch_outliers_parse(const uint8_t* rec, int prec, unsigned long long count_max,
@@ -65,10 +65,10 @@ void launch_reorder(const uint8_t* in, const uint64_t dims[3], int stride, uint8
 void level_kernel_smem_init();
 // k_level.cu: compile-time specialised tiles (16^3, 64x64x1); false = use the generic kernel
 bool launch_level_tiled_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq,
-                                 uint32_t* obm, DevState* st, cudaStream_t s);
+                                 uint32_t* obm, DevState* st, cudaStream_t s, int cfg);
 bool launch_level_tiled_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
                                    const unsigned long long* ocount_dev, double* E, void* out, int prec, DevState* st,
-                                   cudaStream_t s);
+                                   cudaStream_t s, int cfg);
 
 // --- k_tune.cu
 struct TunePlan {

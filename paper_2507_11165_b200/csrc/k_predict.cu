@@ -530,9 +530,9 @@ void level_kernel_smem_init() {
 }
 
 void launch_level_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq, uint32_t* obm,
-                           DevState* st, cudaStream_t s, int* launches) {
+                           DevState* st, cudaStream_t s, int* launches, int cfg) {
   (*launches)++;
-  if (!getenv("HB_GENERIC_LEVELS") && launch_level_tiled_compress(g, field, prec, E, seq, obm, st, s)) return;
+  if (!getenv("HB_GENERIC_LEVELS") && launch_level_tiled_compress(g, field, prec, E, seq, obm, st, s, cfg)) return;
   (*launches)--;
   level_kernel_smem_init();
   const unsigned blocks = (unsigned)((long long)g.ntile[0] * g.ntile[1] * g.ntile[2]);
@@ -548,10 +548,10 @@ void launch_level_compress(const LevelGeom& g, const void* field, int prec, doub
 
 void launch_level_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
                              const unsigned long long* ocount_dev, double* E, void* out, int prec, DevState* st,
-                             cudaStream_t s, int* launches) {
+                             cudaStream_t s, int* launches, int cfg) {
   (*launches)++;
   if (!getenv("HB_GENERIC_LEVELS") &&
-      launch_level_tiled_decompress(g, seq, oidx, oval, ocount_dev, E, out, prec, st, s))
+      launch_level_tiled_decompress(g, seq, oidx, oval, ocount_dev, E, out, prec, st, s, cfg))
     return;
   (*launches)--;
   level_kernel_smem_init();
