@@ -63,10 +63,11 @@ void launch_outliers_parse(const uint8_t* rec, int prec, unsigned long long coun
 void launch_reorder(const uint8_t* in, const uint64_t dims[3], int stride, uint8_t* out, bool inverse,
                     cudaStream_t s, int* launches);
 void level_kernel_smem_init();
-// k_level.cu: compile-time specialised tiles (16^3, 64x64x1); false = use the generic kernel
-bool launch_level_tiled_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq,
+// k_level_{c,d}.cu: column kernels (3D) / 64x64x1 tiles (2D); returns the
+// number of kernels launched, 0 = shape not handled (use the generic kernel)
+int launch_level_tiled_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq,
                                  uint32_t* obm, DevState* st, cudaStream_t s, int cfg);
-bool launch_level_tiled_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
+int launch_level_tiled_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
                                    const unsigned long long* ocount_dev, double* E, void* out, int prec, DevState* st,
                                    cudaStream_t s, int cfg);
 

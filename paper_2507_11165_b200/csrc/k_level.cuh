@@ -1,5 +1,6 @@
-// k_level.cuh -- specialised level kernels (compress + decompress) for the
-// common tile shapes: 16^3 (3D fields) and 64x64x1 (2D fields, d2 == 1).
+// k_level.cuh -- specialised level kernels (compress + decompress) for 2D
+// fields (64x64x1 tiles, d2 == 1); 3D fields use the column kernel k_col.cuh,
+// which shares TileShape, LvArgs, CtaCtx and cp_async from this header.
 //
 // Same algorithm as the generic kernel in k_predict.cu (one CTA per lattice
 // tile, one shared-memory f64 array per parity class, halo recompute, phases
@@ -72,6 +73,7 @@ struct CtaCtx {
   long long d1, d2, e1, e2, s;
   double eb, two_eb, inv_two_eb;
   unsigned long long ocount;
+  bool wE, out0;  // level >= 2 (writes the E lattice) / level 1 (writes the output)
 };
 
 // Eq. 3 slot of a point of class C (bit a = coordinate odd on axis a)
@@ -399,14 +401,9 @@ static inline bool launch_tiled(LevelGeom g, const LvArgs& base, int prec, cudaS
   const bool b0 = g.d[0] > 1, b1 = g.d[1] > 1, b2 = g.d[2] > 1;
   LvArgs A = base;
   if (g.d[0] * g.d[1] * g.d[2] >= (1ll << 31) - (1ll << 24)) return false;  // 32-bit indexing only
-  int kind;
-  if (b0 && b1 && b2)
-    kind = 3;
-  else if (b0 && b1 && !b2)
-    kind = 2;
-  else
-    return false;
-  const int T[3] = {kind == 3 ? 16 : 64, kind == 3 ? 16 : 64, kind == 3 ? 16 : 1};
+  (void)b0, (void)b1;
+  if (!(b0 && b1 && !b2)) return false;  // 3D shapes use the column kernel (k_col.cuh)
+  const int T[3] = {64, 64, 1};
   for (int a = 0; a < 3; a++) {
     g.T[a] = T[a];
     g.ntile[a] = (int)((g.D[a] + T[a] - 1) / T[a]);
@@ -420,19 +417,11 @@ static inline bool launch_tiled(LevelGeom g, const LvArgs& base, int prec, cudaS
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     };
-    set((const void*)k_level_tiled<Tile3, float, DEC>, Tile3::smem_bytes());
-    set((const void*)k_level_tiled<Tile3, double, DEC>, Tile3::smem_bytes());
     set((const void*)k_level_tiled<Tile2, float, DEC>, Tile2::smem_bytes());
     set((const void*)k_level_tiled<Tile2, double, DEC>, Tile2::smem_bytes());
     attr = true;
   }
-  if (kind == 3) {
-    const size_t smem = Tile3::smem_bytes();
-    if (prec == 4)
-      k_level_tiled<Tile3, float, DEC><<<blocks, LV_THREADS, smem, s>>>(A, oid);
-    else
-      k_level_tiled<Tile3, double, DEC><<<blocks, LV_THREADS, smem, s>>>(A, oid);
-  } else {
+  {
     const size_t smem = Tile2::smem_bytes();
     if (prec == 4)
       k_level_tiled<Tile2, float, DEC><<<blocks, LV_THREADS, smem, s>>>(A, oid);

@@ -531,9 +531,12 @@ void level_kernel_smem_init() {
 
 void launch_level_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq, uint32_t* obm,
                            DevState* st, cudaStream_t s, int* launches, int cfg) {
-  (*launches)++;
-  if (!getenv("HB_GENERIC_LEVELS") && launch_level_tiled_compress(g, field, prec, E, seq, obm, st, s, cfg)) return;
-  (*launches)--;
+  if (!getenv("HB_GENERIC_LEVELS")) {
+    if (const int n = launch_level_tiled_compress(g, field, prec, E, seq, obm, st, s, cfg)) {
+      *launches += n;
+      return;
+    }
+  }
   level_kernel_smem_init();
   const unsigned blocks = (unsigned)((long long)g.ntile[0] * g.ntile[1] * g.ntile[2]);
   const size_t smem = (size_t)g.smem_doubles * sizeof(double);
@@ -549,11 +552,12 @@ void launch_level_compress(const LevelGeom& g, const void* field, int prec, doub
 void launch_level_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
                              const unsigned long long* ocount_dev, double* E, void* out, int prec, DevState* st,
                              cudaStream_t s, int* launches, int cfg) {
-  (*launches)++;
-  if (!getenv("HB_GENERIC_LEVELS") &&
-      launch_level_tiled_decompress(g, seq, oidx, oval, ocount_dev, E, out, prec, st, s, cfg))
-    return;
-  (*launches)--;
+  if (!getenv("HB_GENERIC_LEVELS")) {
+    if (const int n = launch_level_tiled_decompress(g, seq, oidx, oval, ocount_dev, E, out, prec, st, s, cfg)) {
+      *launches += n;
+      return;
+    }
+  }
   level_kernel_smem_init();
   const unsigned blocks = (unsigned)((long long)g.ntile[0] * g.ntile[1] * g.ntile[2]);
   const size_t smem = (size_t)g.smem_doubles * sizeof(double);
