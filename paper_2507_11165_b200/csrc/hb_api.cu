@@ -542,6 +542,7 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
   unsigned long long ne = 1;
   for (int a = 0; a < 3; a++) ne *= (dims[a] + 1) / 2;
   const size_t o_E = L.take(ne * 8 + 64);
+  const size_t o_scr = L.take(level_scratch_bytes(dims));
   const size_t o_seq = L.take(N + 128);
   const size_t o_obm = L.take(cdiv(N, 32) * 4 + 64);
   const size_t o_org = L.take(org.size() * 8 + 8);
@@ -640,7 +641,8 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
     for (int level = top; level >= 1; level--) {
       LevelGeom g;
       make_level_geom(dims, level, &g);
-      launch_level_compress(g, dfield, prec, E, seq, obm, st, s, &nl, hcfg[level - 1] & 3);
+      launch_level_compress(g, dfield, prec, E, seq, obm, st, s, &nl, hcfg[level - 1] & 3,
+                            reinterpret_cast<double*>(base + o_scr));
       ctx->mark(lvl_names[level]);
     }
     // 4) outliers straight into the archive (archive.py:65-71)
@@ -767,6 +769,7 @@ int hb_decompress(hb_ctx* ctx, const void* archive, size_t len, void* field_out,
   unsigned long long ne = 1;
   for (int a = 0; a < 3; a++) ne *= (I.dims[a] + 1) / 2;
   const size_t o_E = L.take(ne * 8 + 64);
+  const size_t o_scr = L.take(level_scratch_bytes(I.dims));
   const size_t o_seq = L.take(N + 128);
   const size_t o_oidx = L.take(I.outlier_count * 8 + 64);
   const size_t o_oval = L.take(I.outlier_count * 8 + 64);
@@ -856,7 +859,8 @@ int hb_decompress(hb_ctx* ctx, const void* archive, size_t len, void* field_out,
     for (int level = top; level >= 1; level--) {
       LevelGeom g;
       make_level_geom(I.dims, level, &g);
-      launch_level_decompress(g, codes, oidx, oval, &st->scratch[3], E, out, prec, st, s, &nl, I.cfg[level - 1] & 3);
+      launch_level_decompress(g, codes, oidx, oval, &st->scratch[3], E, out, prec, st, s, &nl, I.cfg[level - 1] & 3,
+                              reinterpret_cast<double*>(base + o_scr));
       static const char* dl_names[5] = {"", "rlevel1", "rlevel2", "rlevel3", "rlevel4"};
       ctx->mark(dl_names[level]);
     }
@@ -898,6 +902,7 @@ int hb_decompose(hb_ctx* ctx, const void* field, int prec, const uint64_t dims[3
   const size_t o_st = L.take(sizeof(DevState));
   const size_t o_field = L.take(N * prec + 64);
   const size_t o_E = L.take(ne * 8 + 64);
+  const size_t o_scr = L.take(level_scratch_bytes(dims));
   const size_t o_seq = L.take(N + 128);
   const size_t o_obm = L.take(cdiv(N, 32) * 4 + 64);
   const size_t o_oidx = L.take(N * 8 + 64);
@@ -927,7 +932,7 @@ int hb_decompose(hb_ctx* ctx, const void* field, int prec, const uint64_t dims[3
     LevelGeom g;
     make_level_geom(dims, level, &g);
     launch_level_compress(g, dfield, prec, E, seq, reinterpret_cast<uint32_t*>(base + o_obm), st, s, &nl,
-                          cfg[level - 1] & 3);
+                          cfg[level - 1] & 3, reinterpret_cast<double*>(base + o_scr));
   }
   launch_outlier_compact(reinterpret_cast<uint32_t*>(base + o_obm), N, dfield, prec, nullptr,
                          reinterpret_cast<uint64_t*>(base + o_oidx), base + o_oval,
@@ -962,6 +967,7 @@ int hb_reconstruct(hb_ctx* ctx, const uint8_t* seq_in, const uint64_t* oidx_in, 
   Layout L;
   const size_t o_st = L.take(sizeof(DevState));
   const size_t o_E = L.take(ne * 8 + 64);
+  const size_t o_scr = L.take(level_scratch_bytes(dims));
   const size_t o_seq = L.take(N + 128);
   const size_t o_oidx = L.take(ocount * 8 + 64);
   const size_t o_ovin = L.take(ocount * prec + 64);
@@ -1011,7 +1017,8 @@ int hb_reconstruct(hb_ctx* ctx, const uint8_t* seq_in, const uint64_t* oidx_in, 
       make_level_geom(dims, level, &g);
       launch_level_decompress(g, base + o_seq, reinterpret_cast<uint64_t*>(base + o_oidx),
                               reinterpret_cast<double*>(base + o_oval), &st->scratch[3],
-                              reinterpret_cast<double*>(base + o_E), out, prec, st, s, &nl, cfg[level - 1] & 3);
+                              reinterpret_cast<double*>(base + o_E), out, prec, st, s, &nl, cfg[level - 1] & 3,
+                              reinterpret_cast<double*>(base + o_scr));
     }
   }
   ctx->launches = nl;

@@ -46,7 +46,8 @@ void launch_anchor_init(const void* field, int prec, const uint64_t dims[3], int
                         uint8_t* anchors_out /*byte-addressed, may be unaligned*/, DevState* st, bool count_hist,
                         cudaStream_t s, int* launches);
 void launch_level_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq,
-                           uint32_t* obitmap, DevState* st, cudaStream_t s, int* launches, int cfg = -1);
+                           uint32_t* obitmap, DevState* st, cudaStream_t s, int* launches, int cfg = -1,
+                           double* scr = nullptr);
 void launch_outlier_compact(const uint32_t* obitmap, unsigned long long n, const void* field, int prec,
                             uint8_t* rec_out /*byte addressed*/, uint64_t* oidx_out, void* oval_out,
                             unsigned long long* lb_status, DevState* st, cudaStream_t s, int* launches);
@@ -54,7 +55,15 @@ void launch_anchor_load(const uint8_t* anchors /*byte addressed*/, int prec, con
                         double* E, cudaStream_t s, int* launches);
 void launch_level_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
                              const unsigned long long* ocount_dev, double* E, void* out, int prec, DevState* st,
-                             cudaStream_t s, int* launches, int cfg = -1);
+                             cudaStream_t s, int* launches, int cfg = -1, double* scr = nullptr);
+// k_pass.cu: 3D levels as dependency passes (no halo recompute); scr = level-1
+// class arrays of level_scratch_bytes(dims).  Returns launches, 0 = not handled.
+size_t level_scratch_bytes(const uint64_t dims[3]);
+int launch_level_pass_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq, uint32_t* obm,
+                               double* scr, DevState* st, cudaStream_t s, int cfg);
+int launch_level_pass_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
+                                 const unsigned long long* ocount_dev, double* E, void* out, int prec, double* scr,
+                                 DevState* st, cudaStream_t s, int cfg);
 void launch_copy_anchors_out(const uint8_t* anchors, int prec, unsigned long long n, void* out, DevState* st,
                              cudaStream_t s, int* launches);
 void launch_outliers_parse(const uint8_t* rec, int prec, unsigned long long count_max,
