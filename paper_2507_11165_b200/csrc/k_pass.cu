@@ -1,0 +1,549 @@
+// k_pass.cu -- level 1 of 3D fields as TMA-fed dependency passes.
+//
+// Level 1 (predictor.py:264-304 at stride 1) holds 7/8 of all targets.  Its
+// parity classes are visited in three dependency steps -- multidim {1,2,4}
+// -> {3,5,6} -> {7}; seq1d {b0} -> {b1, b0|b1} -> {b2, b0|b2, b1|b2, 7} --
+// and each step is one launch that computes every target of its classes
+// exactly once (no halo recompute, no intra-CTA phases).  Reconstructions of
+// classes that a later step reads go to per-class f64 scratch arrays in HBM;
+// the level's source lattice (class 0) is the E array.
+//
+// A CTA owns an 8 x 8 x 32 (x, y, z) block of one class.  One elected thread
+// issues one TMA box load per interpolation axis (the source class with a
+// halo along that axis; out-of-range coordinates are zero-filled by the TMA
+// unit and only ever feed unused stencil taps), completing on an mbarrier,
+// while every thread loads its 8 originals (compress) or 8 codes
+// (decompress) into registers.  Warps = y rows, lanes = z (consecutive in
+// memory and in shared memory), each thread walks 8 targets along x.
+//
+// Reference: predictor.py:181-304 (prediction), :313-329 (quantize),
+// :397-411 (replay), ordering.py:68-84 (Eq. 3 slot of every code).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "hb_common.cuh"
+#include "hb_interp.cuh"
+#include "hb_kernels.h"
+
+namespace hb {
+
+namespace {
+
+constexpr int TX = 8, TY = 8, TZ = 32;
+constexpr int TZH = TZ + 4;  // z-source box z0-2 .. z0+TZ+1 (even start, 16-byte multiple)
+constexpr int T_THREADS = TY * 32;
+constexpr int SLOT = (TX + 3) * TY * TZ;  // doubles per source tile slot (largest box)
+static_assert(TX * TY * TZH <= SLOT && TX * (TY + 3) * TZ <= SLOT, "slot too small");
+
+struct alignas(64) TMaps {
+  CUtensorMap m[6];
+};
+
+struct TPassArgs {
+  LevelGeom g;
+  const void* field;
+  double* E;
+  uint8_t* seq;
+  uint32_t* obm;
+  const uint64_t* oidx;
+  const double* oval;
+  const unsigned long long* ocount;
+  void* out;
+  DevState* st;
+  double* scr;        // class c (1..6) at scr + (c - 1) * cstride, rows padded to even length
+  long long cstride;
+  int ncls, nbx;
+  int cls[4], axm[4];
+  int map[4][3];      // TMA map of the j-th interpolation axis of class k
+};
+
+__device__ __forceinline__ int cdim1(const LevelGeom& g, int cls, int a) {
+  return ((cls >> a) & 1) ? (int)(g.D[a] >> 1) : (int)((g.D[a] + 1) >> 1);
+}
+
+// ---- PTX wrappers: mbarrier + TMA
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned phase) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"((unsigned)__cvta_generic_to_shared(b))
+      : "memory");
+}
+
+// code 0 on decompress: the outlier value at linear index `lin`
+// (predictor.py:400-405; orphan -> ArchiveError).  Rare, kept out of line.
+__device__ __noinline__ double tp_outlier(const uint64_t* oidx, const double* oval, unsigned long long lin,
+                                          unsigned long long cnt, bool& bad) {
+  unsigned long long a0 = 0, a1 = cnt;
+  while (a0 < a1) {
+    const unsigned long long mid = (a0 + a1) >> 1;
+    if (oidx[mid] < lin)
+      a0 = mid + 1;
+    else
+      a1 = mid;
+  }
+  if (a0 < cnt && oidx[a0] == lin) return oval[a0];
+  bad = true;
+  return 0.0;
+}
+
+struct Acc {
+  unsigned h127, h128, h129;
+  bool bad, nf;
+};
+
+// shared-memory geometry of the box of an axis-`a` source: strides of the
+// local x / y index and of one stencil step along a
+struct Tile {
+  int sx, sy, st;
+};
+__device__ __forceinline__ Tile tile_of(int a) {
+  Tile t;
+  if (a == 0) {
+    t.sx = TY * TZ, t.sy = TZ, t.st = TY * TZ;
+  } else if (a == 1) {
+    t.sx = (TY + 3) * TZ, t.sy = TZ, t.st = TZ;
+  } else {
+    t.sx = TY * TZH, t.sy = TZH, t.st = 1;
+  }
+  return t;
+}
+
+// One thread: targets (x0 + i, y, z), i < nx.  INT: every stencil complete.
+template <typename T, bool DEC, int K, bool LINEAR, bool INT>
+__device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, int CLS, int AXM, int x0, int nx,
+                                       int y, int z, int yl, int zl, const T* o, const uint8_t* cd, double eb,
+                                       double two_eb, double inv_two_eb, unsigned long long ocount, unsigned* shist,
+                                       Acc& acc) {
+  const LevelGeom& g = A.g;
+  const int odd0 = CLS & 1, odd1 = (CLS >> 1) & 1, odd2 = (CLS >> 2) & 1;
+  const long long P0 = 2ll * x0 + odd0, P1 = 2ll * y + odd1, P2 = 2ll * z + odd2;
+  const long long lin = (P0 * g.d[1] + P1) * g.d[2] + P2;  // level 1: s = 1
+  long long slot = g.prefix + (P0 * g.D[1] + P1) * g.D[2] + P2 - ((P0 + 1) >> 1) * g.eyez;
+  if (!odd0) {
+    slot -= ((P1 + 1) >> 1) * g.ez;
+    if (!odd1) slot -= (P2 + 1) >> 1;
+  }
+  const int kl0 = (int)g.kl[0], ks0 = (int)g.ks0;
+  uint8_t* sq = A.seq + slot;
+  // reconstruction destination (class 7 is never re-read)
+  const int n1 = cdim1(g, CLS, 1), n2p = (cdim1(g, CLS, 2) + 1) & ~1;
+  double* dp = CLS != 7 ? A.scr + (CLS - 1) * A.cstride + ((long long)x0 * n1 + y) * n2p + z : nullptr;
+  const int dst0 = n1 * n2p;
+  // per-axis shared-memory taps and (boundary) stencil classes
+  const double* tb[K];
+  int tsx[K], tst[K], sax[K], scls[K];
+  {
+    int m = AXM;
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+      const int a = __ffs(m) - 1;
+      m &= m - 1;
+      const Tile t = tile_of(a);
+      sax[j] = a;
+      tb[j] = tiles + j * SLOT + yl * t.sy + zl + (a == 2);  // z box starts one below the first tap
+      tsx[j] = t.sx;
+      tst[j] = t.st;
+      scls[j] = (INT || a == 0) ? (LINEAR ? ST_MID : ST_CUBIC) : classify(a == 1 ? P1 : P2, g.D[a], 1, LINEAR);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TX; i++) {
+    if (i >= nx) break;
+    double pv[K];
+    int ov[K];
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+      int cls = scls[j];
+      if (!INT && sax[j] == 0) cls = classify(P0 + 2 * i, g.D[0], 1, LINEAR);
+      const double* q = tb[j] + i * tsx[j];
+      const int t = tst[j];
+      const double v0 = (INT && LINEAR) ? 0.0 : q[0], v3 = (INT && LINEAR) ? 0.0 : q[3 * t];
+      pv[j] = apply_stencil(INT ? (LINEAR ? ST_MID : ST_CUBIC) : cls, v0, q[t], q[2 * t], v3);
+      ov[j] = INT ? (LINEAR ? 2 : 4) : stencil_order(cls);
+    }
+    const double pred = K == 1 ? pv[0] : combine_axes(K, pv, ov);
+    double r;
+    if (!DEC) {
+      const double ov_ = (double)o[i];
+      const int code = quantize_fast<sizeof(T) == 4>(ov_, pred, eb, two_eb, inv_two_eb, &r);
+      sq[i * ks0] = (uint8_t)code;
+      if (code == 128) {
+        acc.h128++;
+      } else if (code == 127) {
+        acc.h127++;
+      } else if (code == 129) {
+        acc.h129++;
+      } else {
+        atomicAdd(&shist[code], 1u);
+        if (code == 0) {  // outlier (non-finite originals always land here)
+          const unsigned long long li = (unsigned long long)(lin + (long long)i * kl0);
+          atomicOr(&A.obm[li >> 5], 1u << (li & 31));
+          acc.bad |= !isfinite(ov_);
+        }
+      }
+    } else {
+      const int code = cd[i];
+      if (code != 0)
+        r = dequantize(pred, two_eb, code);
+      else
+        r = tp_outlier(A.oidx, A.oval, (unsigned long long)(lin + (long long)i * kl0), ocount, acc.bad);
+      reinterpret_cast<T*>(A.out)[lin + (long long)i * kl0] = (T)r;
+      acc.nf |= !isfinite(r);
+    }
+    if (dp) dp[i * dst0] = r;
+  }
+}
+
+template <typename T, bool DEC, int K, bool LINEAR>
+__global__ void __launch_bounds__(T_THREADS, 2) k_tpass(const __grid_constant__ TPassArgs A,
+                                                         const __grid_constant__ TMaps M) {
+  extern __shared__ __align__(128) double tiles[];
+  __shared__ unsigned shist[256];
+  __shared__ __align__(8) uint64_t bar;
+  const LevelGeom& g = A.g;
+  int k = 0, bx = blockIdx.z;
+  while (k + 1 < A.ncls && bx >= A.nbx) bx -= A.nbx, k++;
+  const int CLS = A.cls[k], AXM = A.axm[k];
+  const int n0 = cdim1(g, CLS, 0), n1 = cdim1(g, CLS, 1), n2 = cdim1(g, CLS, 2);
+  const int x0 = bx * TX, y0 = blockIdx.y * TY, z0 = blockIdx.x * TZ;
+  if (x0 >= n0 || y0 >= n1 || z0 >= n2) return;  // block past this class's extent (uniform)
+  const int yl = threadIdx.x >> 5, zl = threadIdx.x & 31;
+  const int y = y0 + yl, z = z0 + zl;
+  const int nx = min(TX, n0 - x0);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (!DEC)
+    for (int i = threadIdx.x; i < 256; i += T_THREADS) shist[i] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned bytes = 0;
+    int m = AXM;
+    for (int j = 0; j < K; j++) {
+      const int a = __ffs(m) - 1;
+      m &= m - 1;
+      bytes += (a == 2 ? TX * TY * TZH : (a == 1 ? TX * (TY + 3) * TZ : (TX + 3) * TY * TZ)) * 8;
+    }
+    mbar_expect_tx(&bar, bytes);
+    m = AXM;
+    for (int j = 0; j < K; j++) {
+      const int a = __ffs(m) - 1;
+      m &= m - 1;
+      const CUtensorMap* map = &M.m[A.map[k][j]];
+      // the innermost start coordinate must be 16-byte aligned: the z box starts at z0 - 2
+      tma_load_3d(tiles + j * SLOT, map, z0 - 2 * (a == 2), y0 - (a == 1), x0 - (a == 0), &bar);
+    }
+  }
+  // originals / codes of this thread's run, in flight with the boxes
+  const bool live = y < n1 && z < n2;
+  const int odd0 = CLS & 1, odd1 = (CLS >> 1) & 1, odd2 = (CLS >> 2) & 1;
+  T o[TX];
+  uint8_t cd[TX];
+  if (live) {
+    const long long P0 = 2ll * x0 + odd0, P1 = 2ll * y + odd1, P2 = 2ll * z + odd2;
+    if (!DEC) {
+      const T* fp = reinterpret_cast<const T*>(A.field) + (P0 * g.d[1] + P1) * g.d[2] + P2;
+      const int kl0 = (int)g.kl[0];
+#pragma unroll
+      for (int i = 0; i < TX; i++)
+        if (i < nx) o[i] = __ldg(fp + i * kl0);
+    } else {
+      long long slot = g.prefix + (P0 * g.D[1] + P1) * g.D[2] + P2 - ((P0 + 1) >> 1) * g.eyez;
+      if (!odd0) {
+        slot -= ((P1 + 1) >> 1) * g.ez;
+        if (!odd1) slot -= (P2 + 1) >> 1;
+      }
+      const uint8_t* sq = A.seq + slot;
+      const int ks0 = (int)g.ks0;
+#pragma unroll
+      for (int i = 0; i < TX; i++)
+        if (i < nx) cd[i] = __ldg(sq + i * ks0);
+    }
+  }
+  // complete stencils for every target of the block along every axis of AXM
+  bool full = true;
+  {
+    const int lo[3] = {x0, y0, z0};
+    const int hi[3] = {x0 + nx - 1, min(y0 + TY, n1) - 1, min(z0 + TZ, n2) - 1};
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+      if ((AXM >> a) & 1) {
+        const long long Plo = 2ll * lo[a] + 1, Phi = 2ll * hi[a] + 1;
+        full &= LINEAR ? (Phi + 1 < g.D[a]) : (Plo >= 3 && Phi + 3 < g.D[a]);
+      }
+  }
+  const double eb = A.st->eb, two_eb = A.st->two_eb;
+  const double inv_two_eb = __ddiv_rn(1.0, two_eb);
+  const unsigned long long ocount = DEC ? *A.ocount : 0;
+  Acc acc{0u, 0u, 0u, false, false};
+  mbar_wait(&bar, 0);
+  if (live) {
+    if (full)
+      tp_run<T, DEC, K, LINEAR, true>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, o, cd, eb, two_eb, inv_two_eb, ocount,
+                                      shist, acc);
+    else
+      tp_run<T, DEC, K, LINEAR, false>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, o, cd, eb, two_eb, inv_two_eb,
+                                       ocount, shist, acc);
+  }
+  if (DEC && __any_sync(0xffffffffu, acc.nf) && zl == 0) raise_flag(A.st, F_NONFINITE);
+  if (__any_sync(0xffffffffu, acc.bad) && zl == 0) raise_flag(A.st, DEC ? F_ORPHAN : F_NONFINITE);
+  if (!DEC) {
+    const unsigned h7 = __reduce_add_sync(0xffffffffu, acc.h127), h8 = __reduce_add_sync(0xffffffffu, acc.h128),
+                   h9 = __reduce_add_sync(0xffffffffu, acc.h129);
+    if (zl == 0) {
+      if (h7) atomicAdd(&shist[127], h7);
+      if (h8) atomicAdd(&shist[128], h8);
+      if (h9) atomicAdd(&shist[129], h9);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += T_THREADS)
+      if (shist[i]) atomicAdd(&A.st->hist[i], (unsigned long long)shist[i]);
+  }
+}
+
+// level 1 of decompress: the 2-lattice values (E) are output points too
+template <typename T>
+__global__ void k_even_out(const double* __restrict__ E, LevelGeom g, T* out, DevState* st) {
+  const long long n = g.Ed[0] * g.Ed[1] * g.Ed[2];
+  bool nf = false;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long hz = i % g.Ed[2], hy = (i / g.Ed[2]) % g.Ed[1], hx = i / (g.Ed[1] * g.Ed[2]);
+    const double v = E[i];
+    out[((2 * hx) * g.d[1] + 2 * hy) * g.d[2] + 2 * hz] = (T)v;
+    nf |= !isfinite(v);
+  }
+  if (__any_sync(0xffffffffu, nf) && (threadIdx.x & 31) == 0) raise_flag(st, F_NONFINITE);
+}
+
+// ------------------------------------------------------------------ host
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3D f64 array (n0, n1, n2) with rows of n2p doubles; box for an axis-`a` source
+bool make_map(CUtensorMap* m, const double* base, long long n0, long long n1, long long n2, long long n2p, int a) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dim[3] = {(cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)n0};
+  const cuuint64_t str[2] = {(cuuint64_t)(n2p * 8), (cuuint64_t)(n1 * n2p * 8)};
+  const cuuint32_t box[3] = {(cuuint32_t)(a == 2 ? TZH : TZ), (cuuint32_t)(a == 1 ? TY + 3 : TY),
+                             (cuuint32_t)(a == 0 ? TX + 3 : TX)};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dim, str, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct Launch {
+  TPassArgs A;
+  TMaps M;
+  int nmaps;
+};
+
+// map of class `cn` (0 = E) used as an axis-`a` source; reuses an identical one
+int map_for(Launch& L, int cn, int a, int keys[6]) {
+  const int key = cn * 4 + a;
+  for (int i = 0; i < L.nmaps; i++)
+    if (keys[i] == key) return i;
+  if (L.nmaps >= 6) return -1;
+  const LevelGeom& g = L.A.g;
+  long long n[3];
+  for (int b = 0; b < 3; b++) n[b] = ((cn >> b) & 1) ? g.D[b] >> 1 : (g.D[b] + 1) >> 1;
+  bool ok;
+  if (cn == 0)
+    ok = make_map(&L.M.m[L.nmaps], L.A.E, g.Ed[0], g.Ed[1], g.Ed[2], g.Ed[2], a);
+  else
+    ok = make_map(&L.M.m[L.nmaps], L.A.scr + (cn - 1) * L.A.cstride, n[0], n[1], n[2], (n[2] + 1) & ~1ll, a);
+  if (!ok) return -1;
+  keys[L.nmaps] = key;
+  return L.nmaps++;
+}
+
+// builds the maps of one dependency step (false = not expressible as TMA boxes)
+bool plan_step(Launch& L, int K, const int* cls, const int* axm, int n) {
+  TPassArgs& A = L.A;
+  A.ncls = n;
+  L.nmaps = 0;
+  int keys[6] = {-1, -1, -1, -1, -1, -1};
+  long long mx = 0;
+  for (int k = 0; k < n; k++) {
+    A.cls[k] = cls[k];
+    A.axm[k] = axm[k];
+    long long nd[3];
+    for (int a = 0; a < 3; a++) nd[a] = ((cls[k] >> a) & 1) ? A.g.D[a] >> 1 : (A.g.D[a] + 1) >> 1;
+    if (!nd[0] || !nd[1] || !nd[2]) return false;
+    mx = std::max(mx, (nd[0] + TX - 1) / TX);
+    int m = axm[k];
+    for (int j = 0; j < K; j++) {
+      const int a = __builtin_ctz(m);
+      m &= m - 1;
+      const int idx = map_for(L, cls[k] & ~(1 << a), a, keys);
+      if (idx < 0) return false;
+      A.map[k][j] = idx;
+    }
+  }
+  A.nbx = (int)mx;
+  return true;
+}
+
+template <typename T, bool DEC, int K, bool LINEAR>
+void launch_step(const Launch& L, cudaStream_t s, int* launches) {
+  const TPassArgs& A = L.A;
+  long long mz = 0, my = 0;
+  for (int k = 0; k < A.ncls; k++) {
+    const long long n1 = (A.cls[k] & 2) ? A.g.D[1] >> 1 : (A.g.D[1] + 1) >> 1;
+    const long long n2 = (A.cls[k] & 4) ? A.g.D[2] >> 1 : (A.g.D[2] + 1) >> 1;
+    mz = std::max(mz, (n2 + TZ - 1) / TZ);
+    my = std::max(my, (n1 + TY - 1) / TY);
+  }
+  const size_t smem = (size_t)K * SLOT * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute((const void*)k_tpass<T, DEC, K, LINEAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(3 * SLOT * 8));
+    attr = true;
+  }
+  const dim3 grid((unsigned)mz, (unsigned)my, (unsigned)(A.nbx * A.ncls));
+  k_tpass<T, DEC, K, LINEAR><<<grid, T_THREADS, smem, s>>>(A, L.M);
+  (*launches)++;
+}
+
+// the three dependency steps of level 1; every map is built before anything
+// is launched, so a shape TMA cannot express falls back cleanly
+template <typename T, bool DEC, bool LINEAR>
+bool run_passes(const Launch& base, int cfg, cudaStream_t s, int* launches) {
+  Launch L[3] = {base, base, base};
+  int K[3];
+  if ((cfg & 2) == 0) {  // multidim: a class interpolates along all its odd axes
+    const int c1[3] = {1, 2, 4}, c2[3] = {3, 5, 6}, c3[1] = {7};
+    K[0] = 1, K[1] = 2, K[2] = 3;
+    if (!plan_step(L[0], 1, c1, c1, 3) || !plan_step(L[1], 2, c2, c2, 3) || !plan_step(L[2], 3, c3, c3, 1))
+      return false;
+    launch_step<T, DEC, 1, LINEAR>(L[0], s, launches);
+    launch_step<T, DEC, 2, LINEAR>(L[1], s, launches);
+    launch_step<T, DEC, 3, LINEAR>(L[2], s, launches);
+    return true;
+  }
+  // seq1d along seq_order (predictor.py:267-280)
+  const int b0 = 1 << base.A.g.seq_order[0], b1 = 1 << base.A.g.seq_order[1], b2 = 1 << base.A.g.seq_order[2];
+  const int p1c[1] = {b0}, p1a[1] = {b0};
+  const int p2c[2] = {b1, b0 | b1}, p2a[2] = {b1, b1};
+  const int p3c[4] = {b2, b0 | b2, b1 | b2, 7}, p3a[4] = {b2, b2, b2, b2};
+  (void)K;
+  if (!plan_step(L[0], 1, p1c, p1a, 1) || !plan_step(L[1], 1, p2c, p2a, 2) || !plan_step(L[2], 1, p3c, p3a, 4))
+    return false;
+  for (int i = 0; i < 3; i++) launch_step<T, DEC, 1, LINEAR>(L[i], s, launches);
+  return true;
+}
+
+template <typename T, bool DEC>
+bool run_level1(const Launch& L, int cfg, cudaStream_t s, int* launches) {
+  return (cfg & 1) ? run_passes<T, DEC, true>(L, cfg, s, launches) : run_passes<T, DEC, false>(L, cfg, s, launches);
+}
+
+long long class_stride(const LevelGeom& g) {
+  long long n = ((g.D[0] + 1) / 2) * ((g.D[1] + 1) / 2) * (((g.D[2] + 1) / 2 + 1) & ~1ll);
+  return (n + 15) & ~15ll;  // keeps every class array 128-byte aligned
+}
+
+// level 1 of a 3D field whose E rows are 16-byte multiples (TMA global strides)
+bool tpass_ok(const LevelGeom& g, const double* E, const double* scr, int cfg) {
+  return cfg >= 0 && scr && g.level == 1 && g.d[0] > 1 && g.d[1] > 1 && g.d[2] > 1 && (g.Ed[2] % 2) == 0 &&
+         (reinterpret_cast<uintptr_t>(E) & 15) == 0 && (reinterpret_cast<uintptr_t>(scr) & 127) == 0 &&
+         !getenv("HB_TILED_LEVELS") && encode_fn() != nullptr;
+}
+
+}  // namespace
+
+size_t level_scratch_bytes(const uint64_t dims[3]) {
+  LevelGeom g;
+  make_level_geom(dims, 1, &g);
+  return (size_t)6 * class_stride(g) * 8 + 256;
+}
+
+int launch_level_pass_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq, uint32_t* obm,
+                               double* scr, DevState* st, cudaStream_t s, int cfg) {
+  if (!tpass_ok(g, E, scr, cfg)) return 0;
+  Launch L{};
+  L.A.g = g;
+  L.A.field = field;
+  L.A.E = E;
+  L.A.seq = seq;
+  L.A.obm = obm;
+  L.A.st = st;
+  L.A.scr = scr;
+  L.A.cstride = class_stride(g);
+  int n = 0;
+  prec == 4 ? run_level1<float, false>(L, cfg, s, &n) : run_level1<double, false>(L, cfg, s, &n);
+  return n;
+}
+
+int launch_level_pass_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
+                                 const unsigned long long* ocount_dev, double* E, void* out, int prec, double* scr,
+                                 DevState* st, cudaStream_t s, int cfg) {
+  if (!tpass_ok(g, E, scr, cfg)) return 0;
+  Launch L{};
+  L.A.g = g;
+  L.A.E = E;
+  L.A.seq = const_cast<uint8_t*>(seq);
+  L.A.oidx = oidx;
+  L.A.oval = oval;
+  L.A.ocount = ocount_dev;
+  L.A.out = out;
+  L.A.st = st;
+  L.A.scr = scr;
+  L.A.cstride = class_stride(g);
+  int n = 0;
+  // the passes plan every TMA map before launching anything (false = nothing launched)
+  if (!(prec == 4 ? run_level1<float, true>(L, cfg, s, &n) : run_level1<double, true>(L, cfg, s, &n))) return 0;
+  {
+    const long long ne = g.Ed[0] * g.Ed[1] * g.Ed[2];
+    const unsigned blocks = (unsigned)std::min<long long>((ne + 255) / 256, 148 * 16);
+    if (prec == 4)
+      k_even_out<float><<<blocks, 256, 0, s>>>(E, g, reinterpret_cast<float*>(out), st);
+    else
+      k_even_out<double><<<blocks, 256, 0, s>>>(E, g, reinterpret_cast<double*>(out), st);
+    n++;
+  }
+  return n;
+}
+
+}  // namespace hb
