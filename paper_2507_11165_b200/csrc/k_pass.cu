@@ -57,6 +57,7 @@ struct TPassArgs {
   double* scr;        // class c (1..6) at scr + (c - 1) * cstride, rows padded to even length
   long long cstride;
   int ncls, nbx;
+  int pairs;          // decompress, multidim, even d2: odd-z classes write (z-1, z) output pairs
   int cls[4], axm[4];
   int map[4][3];      // TMA map of the j-th interpolation axis of class k
 };
@@ -177,12 +178,14 @@ __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, 
     if (i >= nx) break;
     double pv[K];
     int ov[K];
+    double zpart = 0.0;  // the z-source value at z (the output partner of an odd-z target)
 #pragma unroll
     for (int j = 0; j < K; j++) {
       int cls = scls[j];
       if (!INT && sax[j] == 0) cls = classify(P0 + 2 * i, g.D[0], 1, LINEAR);
       const double* q = tb[j] + i * tsx[j];
       const int t = tst[j];
+      if (DEC && sax[j] == 2) zpart = q[t];
       const double v0 = (INT && LINEAR) ? 0.0 : q[0], v3 = (INT && LINEAR) ? 0.0 : q[3 * t];
       pv[j] = apply_stencil(INT ? (LINEAR ? ST_MID : ST_CUBIC) : cls, v0, q[t], q[2 * t], v3);
       ov[j] = INT ? (LINEAR ? 2 : 4) : stencil_order(cls);
@@ -213,8 +216,17 @@ __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, 
         r = dequantize(pred, two_eb, code);
       else
         r = tp_outlier(A.oidx, A.oval, (unsigned long long)(lin + (long long)i * kl0), ocount, acc.bad);
-      reinterpret_cast<T*>(A.out)[lin + (long long)i * kl0] = (T)r;
-      acc.nf |= !isfinite(r);
+      T* op = reinterpret_cast<T*>(A.out) + lin + (long long)i * kl0;
+      if (!A.pairs) {
+        *op = (T)r;
+        acc.nf |= !isfinite(r);
+      } else if (odd2) {  // one aligned store covers (z-1, z); the even-z classes write nothing
+        if (sizeof(T) == 4)
+          *reinterpret_cast<float2*>(op - 1) = make_float2((float)zpart, (float)r);
+        else
+          *reinterpret_cast<double2*>(op - 1) = make_double2(zpart, r);
+        acc.nf |= !isfinite(r) || !isfinite(zpart);
+      }
     }
     if (dp) dp[i * dst0] = r;
   }
@@ -531,10 +543,11 @@ int launch_level_pass_decompress(const LevelGeom& g, const uint8_t* seq, const u
   L.A.st = st;
   L.A.scr = scr;
   L.A.cstride = class_stride(g);
+  L.A.pairs = (cfg & 2) == 0 && (g.d[2] % 2) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
   int n = 0;
   // the passes plan every TMA map before launching anything (false = nothing launched)
   if (!(prec == 4 ? run_level1<float, true>(L, cfg, s, &n) : run_level1<double, true>(L, cfg, s, &n))) return 0;
-  {
+  if (!L.A.pairs) {  // class 0 (the E lattice) is written by its odd-z partners when pairing
     const long long ne = g.Ed[0] * g.Ed[1] * g.Ed[2];
     const unsigned blocks = (unsigned)std::min<long long>((ne + 255) / 256, 148 * 16);
     if (prec == 4)
