@@ -1,12 +1,14 @@
-// k_pass.cu -- level 1 of 3D fields as TMA-fed dependency passes.
+// k_pass.cu -- the levels of 3D fields as TMA-fed dependency passes.
 //
-// Level 1 (predictor.py:264-304 at stride 1) holds 7/8 of all targets.  Its
-// parity classes are visited in three dependency steps -- multidim {1,2,4}
-// -> {3,5,6} -> {7}; seq1d {b0} -> {b1, b0|b1} -> {b2, b0|b2, b1|b2, 7} --
-// and each step is one launch that computes every target of its classes
-// exactly once (no halo recompute, no intra-CTA phases).  Reconstructions of
-// classes that a later step reads go to per-class f64 scratch arrays in HBM;
-// the level's source lattice (class 0) is the E array.
+// A level (predictor.py:264-304) visits the parity classes of its lattice in
+// three dependency steps -- multidim {1,2,4} -> {3,5,6} -> {7}; seq1d {b0} ->
+// {b1, b0|b1} -> {b2, b0|b2, b1|b2, 7} -- and each step is one launch that
+// computes every target of its classes exactly once (no halo recompute, no
+// intra-CTA phases).  Reconstructions of classes that a later step reads go
+// to dense per-class f64 scratch arrays in HBM.  The level's source lattice
+// (class 0) is the E array itself at level 1 (unit stride, even rows) and a
+// dense gathered copy otherwise; levels >= 2 also write their targets into E,
+// where they form the next level's lattice.
 //
 // A CTA owns an 8 x 8 x 32 (x, y, z) block of one class.  One elected thread
 // issues one TMA box load per interpolation axis (the source class with a
@@ -54,8 +56,8 @@ struct TPassArgs {
   const unsigned long long* ocount;
   void* out;
   DevState* st;
-  double* scr;        // class c (1..6) at scr + (c - 1) * cstride, rows padded to even length
-  long long cstride;
+  double* scr;        // class c (1..6) at scr + (c - 1) * cstride, rows padded to even length;
+  long long cstride;  // gathered class 0 (when used) at scr + 6 * cstride
   int ncls, nbx;
   int pairs;          // decompress, multidim, even d2: odd-z classes write (z-1, z) output pairs
   int cls[4], axm[4];
@@ -136,7 +138,7 @@ __device__ __forceinline__ Tile tile_of(int a) {
 }
 
 // One thread: targets (x0 + i, y, z), i < nx.  INT: every stencil complete.
-template <typename T, bool DEC, int K, bool LINEAR, bool INT>
+template <typename T, bool DEC, int K, bool LINEAR, bool INT, bool LV1>
 __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, int CLS, int AXM, int x0, int nx,
                                        int y, int z, int yl, int zl, const T* o, const uint8_t* cd, double eb,
                                        double two_eb, double inv_two_eb, unsigned long long ocount, unsigned* shist,
@@ -144,7 +146,8 @@ __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, 
   const LevelGeom& g = A.g;
   const int odd0 = CLS & 1, odd1 = (CLS >> 1) & 1, odd2 = (CLS >> 2) & 1;
   const long long P0 = 2ll * x0 + odd0, P1 = 2ll * y + odd1, P2 = 2ll * z + odd2;
-  const long long lin = (P0 * g.d[1] + P1) * g.d[2] + P2;  // level 1: s = 1
+  const long long sg = LV1 ? 1 : g.s;
+  const long long lin = ((P0 * sg) * g.d[1] + P1 * sg) * g.d[2] + P2 * sg;
   long long slot = g.prefix + (P0 * g.D[1] + P1) * g.D[2] + P2 - ((P0 + 1) >> 1) * g.eyez;
   if (!odd0) {
     slot -= ((P1 + 1) >> 1) * g.ez;
@@ -156,6 +159,10 @@ __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, 
   const int n1 = cdim1(g, CLS, 1), n2p = (cdim1(g, CLS, 2) + 1) & ~1;
   double* dp = CLS != 7 ? A.scr + (CLS - 1) * A.cstride + ((long long)x0 * n1 + y) * n2p + z : nullptr;
   const int dst0 = n1 * n2p;
+  // levels >= 2: the target is also a point of the next level's lattice (E)
+  double* ep = !LV1 ? A.E + ((P0 * sg) >> 1) * g.Ed[1] * g.Ed[2] + ((P1 * sg) >> 1) * g.Ed[2] + ((P2 * sg) >> 1)
+                            : nullptr;
+  const int ke0 = (int)g.ke[0];
   // per-axis shared-memory taps and (boundary) stencil classes
   const double* tb[K];
   int tsx[K], tst[K], sax[K], scls[K];
@@ -217,7 +224,9 @@ __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, 
       else
         r = tp_outlier(A.oidx, A.oval, (unsigned long long)(lin + (long long)i * kl0), ocount, acc.bad);
       T* op = reinterpret_cast<T*>(A.out) + lin + (long long)i * kl0;
-      if (!A.pairs) {
+      if (!LV1) {
+        // not an output point yet: the value lives on in E
+      } else if (!A.pairs) {
         *op = (T)r;
         acc.nf |= !isfinite(r);
       } else if (odd2) {  // one aligned store covers (z-1, z); the even-z classes write nothing
@@ -229,10 +238,11 @@ __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, 
       }
     }
     if (dp) dp[i * dst0] = r;
+    if (!LV1) ep[i * ke0] = r;
   }
 }
 
-template <typename T, bool DEC, int K, bool LINEAR>
+template <typename T, bool DEC, int K, bool LINEAR, bool LV1>
 __global__ void __launch_bounds__(T_THREADS, 2) k_tpass(const __grid_constant__ TPassArgs A,
                                                          const __grid_constant__ TMaps M) {
   extern __shared__ __align__(128) double tiles[];
@@ -282,7 +292,8 @@ __global__ void __launch_bounds__(T_THREADS, 2) k_tpass(const __grid_constant__ 
   if (live) {
     const long long P0 = 2ll * x0 + odd0, P1 = 2ll * y + odd1, P2 = 2ll * z + odd2;
     if (!DEC) {
-      const T* fp = reinterpret_cast<const T*>(A.field) + (P0 * g.d[1] + P1) * g.d[2] + P2;
+      const long long sg = LV1 ? 1 : g.s;
+      const T* fp = reinterpret_cast<const T*>(A.field) + ((P0 * sg) * g.d[1] + P1 * sg) * g.d[2] + P2 * sg;
       const int kl0 = (int)g.kl[0];
 #pragma unroll
       for (int i = 0; i < TX; i++)
@@ -319,10 +330,10 @@ __global__ void __launch_bounds__(T_THREADS, 2) k_tpass(const __grid_constant__ 
   mbar_wait(&bar, 0);
   if (live) {
     if (full)
-      tp_run<T, DEC, K, LINEAR, true>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, o, cd, eb, two_eb, inv_two_eb, ocount,
+      tp_run<T, DEC, K, LINEAR, true, LV1>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, o, cd, eb, two_eb, inv_two_eb, ocount,
                                       shist, acc);
     else
-      tp_run<T, DEC, K, LINEAR, false>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, o, cd, eb, two_eb, inv_two_eb,
+      tp_run<T, DEC, K, LINEAR, false, LV1>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, o, cd, eb, two_eb, inv_two_eb,
                                        ocount, shist, acc);
   }
   if (DEC && __any_sync(0xffffffffu, acc.nf) && zl == 0) raise_flag(A.st, F_NONFINITE);
@@ -353,6 +364,17 @@ __global__ void k_even_out(const double* __restrict__ E, LevelGeom g, T* out, De
     nf |= !isfinite(v);
   }
   if (__any_sync(0xffffffffu, nf) && (threadIdx.x & 31) == 0) raise_flag(st, F_NONFINITE);
+}
+
+// class 0 of a level with stride s >= 2 (or odd E rows): dense copy of the
+// 2s-lattice out of E, rows padded to even length (TMA global strides)
+__global__ void k_gather0(const double* __restrict__ E, LevelGeom g, double* __restrict__ C0, long long n1, long long n2,
+                          long long n2p, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long w = i % n2p, v = (i / n2p) % n1, u = i / (n2p * n1);
+    if (w >= n2) continue;
+    C0[i] = E[((u * g.s) * g.Ed[1] + v * g.s) * g.Ed[2] + w * g.s];
+  }
 }
 
 // ------------------------------------------------------------------ host
@@ -388,6 +410,7 @@ struct Launch {
   TPassArgs A;
   TMaps M;
   int nmaps;
+  bool gathered;  // class 0 read from the dense copy at scr + 6 * cstride
 };
 
 // map of class `cn` (0 = E) used as an axis-`a` source; reuses an identical one
@@ -400,8 +423,10 @@ int map_for(Launch& L, int cn, int a, int keys[6]) {
   long long n[3];
   for (int b = 0; b < 3; b++) n[b] = ((cn >> b) & 1) ? g.D[b] >> 1 : (g.D[b] + 1) >> 1;
   bool ok;
-  if (cn == 0)
+  if (cn == 0 && !L.gathered)
     ok = make_map(&L.M.m[L.nmaps], L.A.E, g.Ed[0], g.Ed[1], g.Ed[2], g.Ed[2], a);
+  else if (cn == 0)
+    ok = make_map(&L.M.m[L.nmaps], L.A.scr + 6 * L.A.cstride, n[0], n[1], n[2], (n[2] + 1) & ~1ll, a);
   else
     ok = make_map(&L.M.m[L.nmaps], L.A.scr + (cn - 1) * L.A.cstride, n[0], n[1], n[2], (n[2] + 1) & ~1ll, a);
   if (!ok) return -1;
@@ -436,7 +461,7 @@ bool plan_step(Launch& L, int K, const int* cls, const int* axm, int n) {
   return true;
 }
 
-template <typename T, bool DEC, int K, bool LINEAR>
+template <typename T, bool DEC, int K, bool LINEAR, bool LV1>
 void launch_step(const Launch& L, cudaStream_t s, int* launches) {
   const TPassArgs& A = L.A;
   long long mz = 0, my = 0;
@@ -449,18 +474,18 @@ void launch_step(const Launch& L, cudaStream_t s, int* launches) {
   const size_t smem = (size_t)K * SLOT * 8;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute((const void*)k_tpass<T, DEC, K, LINEAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute((const void*)k_tpass<T, DEC, K, LINEAR, LV1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(3 * SLOT * 8));
     attr = true;
   }
   const dim3 grid((unsigned)mz, (unsigned)my, (unsigned)(A.nbx * A.ncls));
-  k_tpass<T, DEC, K, LINEAR><<<grid, T_THREADS, smem, s>>>(A, L.M);
+  k_tpass<T, DEC, K, LINEAR, LV1><<<grid, T_THREADS, smem, s>>>(A, L.M);
   (*launches)++;
 }
 
 // the three dependency steps of level 1; every map is built before anything
 // is launched, so a shape TMA cannot express falls back cleanly
-template <typename T, bool DEC, bool LINEAR>
+template <typename T, bool DEC, bool LINEAR, bool LV1>
 bool run_passes(const Launch& base, int cfg, cudaStream_t s, int* launches) {
   Launch L[3] = {base, base, base};
   int K[3];
@@ -469,9 +494,9 @@ bool run_passes(const Launch& base, int cfg, cudaStream_t s, int* launches) {
     K[0] = 1, K[1] = 2, K[2] = 3;
     if (!plan_step(L[0], 1, c1, c1, 3) || !plan_step(L[1], 2, c2, c2, 3) || !plan_step(L[2], 3, c3, c3, 1))
       return false;
-    launch_step<T, DEC, 1, LINEAR>(L[0], s, launches);
-    launch_step<T, DEC, 2, LINEAR>(L[1], s, launches);
-    launch_step<T, DEC, 3, LINEAR>(L[2], s, launches);
+    launch_step<T, DEC, 1, LINEAR, LV1>(L[0], s, launches);
+    launch_step<T, DEC, 2, LINEAR, LV1>(L[1], s, launches);
+    launch_step<T, DEC, 3, LINEAR, LV1>(L[2], s, launches);
     return true;
   }
   // seq1d along seq_order (predictor.py:267-280)
@@ -482,13 +507,17 @@ bool run_passes(const Launch& base, int cfg, cudaStream_t s, int* launches) {
   (void)K;
   if (!plan_step(L[0], 1, p1c, p1a, 1) || !plan_step(L[1], 1, p2c, p2a, 2) || !plan_step(L[2], 1, p3c, p3a, 4))
     return false;
-  for (int i = 0; i < 3; i++) launch_step<T, DEC, 1, LINEAR>(L[i], s, launches);
+  for (int i = 0; i < 3; i++) launch_step<T, DEC, 1, LINEAR, LV1>(L[i], s, launches);
   return true;
 }
 
 template <typename T, bool DEC>
-bool run_level1(const Launch& L, int cfg, cudaStream_t s, int* launches) {
-  return (cfg & 1) ? run_passes<T, DEC, true>(L, cfg, s, launches) : run_passes<T, DEC, false>(L, cfg, s, launches);
+bool run_level(const Launch& L, int cfg, cudaStream_t s, int* launches) {
+  if (L.A.g.level == 1)
+    return (cfg & 1) ? run_passes<T, DEC, true, true>(L, cfg, s, launches)
+                     : run_passes<T, DEC, false, true>(L, cfg, s, launches);
+  return (cfg & 1) ? run_passes<T, DEC, true, false>(L, cfg, s, launches)
+                   : run_passes<T, DEC, false, false>(L, cfg, s, launches);
 }
 
 long long class_stride(const LevelGeom& g) {
@@ -498,17 +527,30 @@ long long class_stride(const LevelGeom& g) {
 
 // level 1 of a 3D field whose E rows are 16-byte multiples (TMA global strides)
 bool tpass_ok(const LevelGeom& g, const double* E, const double* scr, int cfg) {
-  return cfg >= 0 && scr && g.level == 1 && g.d[0] > 1 && g.d[1] > 1 && g.d[2] > 1 && (g.Ed[2] % 2) == 0 &&
-         (reinterpret_cast<uintptr_t>(E) & 15) == 0 && (reinterpret_cast<uintptr_t>(scr) & 127) == 0 &&
-         !getenv("HB_TILED_LEVELS") && encode_fn() != nullptr;
+  return cfg >= 0 && scr && g.d[0] > 1 && g.d[1] > 1 && g.d[2] > 1 && (reinterpret_cast<uintptr_t>(E) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(scr) & 127) == 0 && !getenv("HB_TILED_LEVELS") && encode_fn() != nullptr;
+}
+
+// level 1 with even E rows reads class 0 straight from E; otherwise gather it
+void prepare_class0(Launch& L, cudaStream_t s, int* launches) {
+  const LevelGeom& g = L.A.g;
+  L.gathered = !(g.level == 1 && (g.Ed[2] % 2) == 0);
+  if (!L.gathered) return;
+  const long long n0 = (g.D[0] + 1) / 2, n1 = (g.D[1] + 1) / 2, n2 = (g.D[2] + 1) / 2, n2p = (n2 + 1) & ~1ll;
+  const long long n = n0 * n1 * n2p;
+  const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148 * 16);
+  k_gather0<<<blocks, 256, 0, s>>>(L.A.E, g, L.A.scr + 6 * L.A.cstride, n1, n2, n2p, n);
+  (*launches)++;
 }
 
 }  // namespace
 
 size_t level_scratch_bytes(const uint64_t dims[3]) {
+  // level 1: six class arrays + (odd E rows) the gathered lattice; a level
+  // L >= 2 needs seven arrays of 1/8^(L-1) the size
   LevelGeom g;
   make_level_geom(dims, 1, &g);
-  return (size_t)6 * class_stride(g) * 8 + 256;
+  return (size_t)7 * class_stride(g) * 8 + 256;
 }
 
 int launch_level_pass_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq, uint32_t* obm,
@@ -523,8 +565,15 @@ int launch_level_pass_compress(const LevelGeom& g, const void* field, int prec, 
   L.A.st = st;
   L.A.scr = scr;
   L.A.cstride = class_stride(g);
+  L.gathered = !(g.level == 1 && (g.Ed[2] % 2) == 0);
+  {  // every map must be expressible before anything is launched
+    Launch t = L;
+    const int c1[1] = {1};
+    if (!plan_step(t, 1, c1, c1, 1)) return 0;
+  }
   int n = 0;
-  prec == 4 ? run_level1<float, false>(L, cfg, s, &n) : run_level1<double, false>(L, cfg, s, &n);
+  prepare_class0(L, s, &n);  // harmless if the passes below cannot run (scratch only)
+  if (!(prec == 4 ? run_level<float, false>(L, cfg, s, &n) : run_level<double, false>(L, cfg, s, &n))) return 0;
   return n;
 }
 
@@ -543,11 +592,17 @@ int launch_level_pass_decompress(const LevelGeom& g, const uint8_t* seq, const u
   L.A.st = st;
   L.A.scr = scr;
   L.A.cstride = class_stride(g);
-  L.A.pairs = (cfg & 2) == 0 && (g.d[2] % 2) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  L.A.pairs = g.level == 1 && (cfg & 2) == 0 && (g.d[2] % 2) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  L.gathered = !(g.level == 1 && (g.Ed[2] % 2) == 0);
+  {  // every map must be expressible before anything is launched
+    Launch t = L;
+    const int c1[1] = {1};
+    if (!plan_step(t, 1, c1, c1, 1)) return 0;
+  }
   int n = 0;
-  // the passes plan every TMA map before launching anything (false = nothing launched)
-  if (!(prec == 4 ? run_level1<float, true>(L, cfg, s, &n) : run_level1<double, true>(L, cfg, s, &n))) return 0;
-  if (!L.A.pairs) {  // class 0 (the E lattice) is written by its odd-z partners when pairing
+  prepare_class0(L, s, &n);  // harmless if the passes below cannot run (scratch only)
+  if (!(prec == 4 ? run_level<float, true>(L, cfg, s, &n) : run_level<double, true>(L, cfg, s, &n))) return 0;
+  if (g.level == 1 && !L.A.pairs) {  // class 0 (the E lattice) is written by its odd-z partners when pairing
     const long long ne = g.Ed[0] * g.Ed[1] * g.Ed[2];
     const unsigned blocks = (unsigned)std::min<long long>((ne + 255) / 256, 148 * 16);
     if (prec == 4)
