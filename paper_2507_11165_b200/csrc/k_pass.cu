@@ -140,19 +140,13 @@ __device__ __forceinline__ Tile tile_of(int a) {
 // One thread: targets (x0 + i, y, z), i < nx.  INT: every stencil complete.
 template <typename T, bool DEC, int K, bool LINEAR, bool INT, bool LV1>
 __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, int CLS, int AXM, int x0, int nx,
-                                       int y, int z, int yl, int zl, const T* o, const uint8_t* cd, double eb,
-                                       double two_eb, double inv_two_eb, unsigned long long ocount, unsigned* shist,
-                                       Acc& acc) {
+                                       int y, int z, int yl, int zl, long long lin, long long slot, const T* o,
+                                       const uint8_t* cd, double eb, double two_eb, double inv_two_eb,
+                                       unsigned long long ocount, unsigned* shist, Acc& acc) {
   const LevelGeom& g = A.g;
   const int odd0 = CLS & 1, odd1 = (CLS >> 1) & 1, odd2 = (CLS >> 2) & 1;
   const long long P0 = 2ll * x0 + odd0, P1 = 2ll * y + odd1, P2 = 2ll * z + odd2;
   const long long sg = LV1 ? 1 : g.s;
-  const long long lin = ((P0 * sg) * g.d[1] + P1 * sg) * g.d[2] + P2 * sg;
-  long long slot = g.prefix + (P0 * g.D[1] + P1) * g.D[2] + P2 - ((P0 + 1) >> 1) * g.eyez;
-  if (!odd0) {
-    slot -= ((P1 + 1) >> 1) * g.ez;
-    if (!odd1) slot -= (P2 + 1) >> 1;
-  }
   const int kl0 = (int)g.kl[0], ks0 = (int)g.ks0;
   uint8_t* sq = A.seq + slot;
   // reconstruction destination (class 7 is never re-read)
@@ -249,8 +243,10 @@ __global__ void __launch_bounds__(T_THREADS, 2) k_tpass(const __grid_constant__ 
   __shared__ unsigned shist[256];
   __shared__ __align__(8) uint64_t bar;
   const LevelGeom& g = A.g;
-  int k = 0, bx = blockIdx.z;
-  while (k + 1 < A.ncls && bx >= A.nbx) bx -= A.nbx, k++;
+  // class-minor block order: the classes of one x slab run back to back, so
+  // the source tiles they share (and the halo rows of their neighbours)
+  // are still in L2 when the second reader comes
+  const int bx = (int)blockIdx.z / A.ncls, k = (int)blockIdx.z - bx * A.ncls;
   const int CLS = A.cls[k], AXM = A.axm[k];
   const int n0 = cdim1(g, CLS, 0), n1 = cdim1(g, CLS, 1), n2 = cdim1(g, CLS, 2);
   const int x0 = bx * TX, y0 = blockIdx.y * TY, z0 = blockIdx.x * TZ;
@@ -258,10 +254,16 @@ __global__ void __launch_bounds__(T_THREADS, 2) k_tpass(const __grid_constant__ 
   const int yl = threadIdx.x >> 5, zl = threadIdx.x & 31;
   const int y = y0 + yl, z = z0 + zl;
   const int nx = min(TX, n0 - x0);
+  __shared__ double s_eb[3];
+  __shared__ unsigned long long s_ocount;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    s_eb[0] = A.st->eb;
+    s_eb[1] = A.st->two_eb;
+    s_eb[2] = __ddiv_rn(1.0, s_eb[1]);  // one IEEE division per block
+    s_ocount = DEC ? *A.ocount : 0;
   }
   if (!DEC)
     for (int i = threadIdx.x; i < 256; i += T_THREADS) shist[i] = 0;
@@ -289,21 +291,23 @@ __global__ void __launch_bounds__(T_THREADS, 2) k_tpass(const __grid_constant__ 
   const int odd0 = CLS & 1, odd1 = (CLS >> 1) & 1, odd2 = (CLS >> 2) & 1;
   T o[TX];
   uint8_t cd[TX];
+  // element index and Eq. 3 slot of the run's first target (ordering.py:68-84)
+  const long long P0 = 2ll * x0 + odd0, P1 = 2ll * y + odd1, P2 = 2ll * z + odd2;
+  const long long sg = LV1 ? 1 : g.s;
+  const long long lin = ((P0 * sg) * g.d[1] + P1 * sg) * g.d[2] + P2 * sg;
+  long long slot = g.prefix + (P0 * g.D[1] + P1) * g.D[2] + P2 - ((P0 + 1) >> 1) * g.eyez;
+  if (!odd0) {
+    slot -= ((P1 + 1) >> 1) * g.ez;
+    if (!odd1) slot -= (P2 + 1) >> 1;
+  }
   if (live) {
-    const long long P0 = 2ll * x0 + odd0, P1 = 2ll * y + odd1, P2 = 2ll * z + odd2;
     if (!DEC) {
-      const long long sg = LV1 ? 1 : g.s;
-      const T* fp = reinterpret_cast<const T*>(A.field) + ((P0 * sg) * g.d[1] + P1 * sg) * g.d[2] + P2 * sg;
+      const T* fp = reinterpret_cast<const T*>(A.field) + lin;
       const int kl0 = (int)g.kl[0];
 #pragma unroll
       for (int i = 0; i < TX; i++)
         if (i < nx) o[i] = __ldg(fp + i * kl0);
     } else {
-      long long slot = g.prefix + (P0 * g.D[1] + P1) * g.D[2] + P2 - ((P0 + 1) >> 1) * g.eyez;
-      if (!odd0) {
-        slot -= ((P1 + 1) >> 1) * g.ez;
-        if (!odd1) slot -= (P2 + 1) >> 1;
-      }
       const uint8_t* sq = A.seq + slot;
       const int ks0 = (int)g.ks0;
 #pragma unroll
@@ -323,17 +327,16 @@ __global__ void __launch_bounds__(T_THREADS, 2) k_tpass(const __grid_constant__ 
         full &= LINEAR ? (Phi + 1 < g.D[a]) : (Plo >= 3 && Phi + 3 < g.D[a]);
       }
   }
-  const double eb = A.st->eb, two_eb = A.st->two_eb;
-  const double inv_two_eb = __ddiv_rn(1.0, two_eb);
-  const unsigned long long ocount = DEC ? *A.ocount : 0;
+  const double eb = s_eb[0], two_eb = s_eb[1], inv_two_eb = s_eb[2];
+  const unsigned long long ocount = s_ocount;
   Acc acc{0u, 0u, 0u, false, false};
   mbar_wait(&bar, 0);
   if (live) {
     if (full)
-      tp_run<T, DEC, K, LINEAR, true, LV1>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, o, cd, eb, two_eb, inv_two_eb, ocount,
+      tp_run<T, DEC, K, LINEAR, true, LV1>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb, two_eb, inv_two_eb, ocount,
                                       shist, acc);
     else
-      tp_run<T, DEC, K, LINEAR, false, LV1>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, o, cd, eb, two_eb, inv_two_eb,
+      tp_run<T, DEC, K, LINEAR, false, LV1>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb, two_eb, inv_two_eb,
                                        ocount, shist, acc);
   }
   if (DEC && __any_sync(0xffffffffu, acc.nf) && zl == 0) raise_flag(A.st, F_NONFINITE);
