@@ -1275,35 +1275,69 @@ __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsi
   }
 }
 
+// MSB-first bit reader over the payload: refills 32 bits at a time from
+// aligned big-endian words (one load per 32 bits instead of one per byte).
+// Invariant after every operation: nb >= 33 valid bits at the top of buf.
 struct BitReader {
-  const uint8_t* p;
-  unsigned long long nbytes;
-  unsigned long long byte;  // next byte to load
-  uint64_t buf;             // MSB-aligned
+  const uint32_t* w;          // aligned word base (at or just before the payload)
+  unsigned long long wi, nw;  // next word, words holding payload bytes
+  unsigned long long endb;    // payload end in bytes from w
+  uint64_t buf;               // MSB-aligned
   int nb;
+  __device__ __forceinline__ uint32_t word(unsigned long long i) const {
+    if (i + 1 < nw) return __byte_perm(__ldg(w + i), 0, 0x0123);
+    // the last (possibly partial) word: byte loads, nothing past the payload
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(w);
+    uint32_t x = 0;
+    for (int k = 0; k < 4; k++) {
+      const unsigned long long j = 4 * i + k;
+      x = (x << 8) | (j < endb ? b[j] : 0u);
+    }
+    return x;
+  }
   __device__ void init(const uint8_t* pay, unsigned long long plen, unsigned long long pos) {
-    p = pay;
-    nbytes = plen;
-    byte = pos >> 3;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(pay);
+    const int sh = (int)(a & 3);
+    w = reinterpret_cast<const uint32_t*>(a - sh);
+    endb = plen + sh;
+    nw = (endb + 3) >> 2;
+    const unsigned long long bp = pos + 8ull * sh;
+    wi = bp >> 5;
     buf = 0;
     nb = 0;
     refill();
-    const int skip = (int)(pos & 7);
+    const int skip = (int)(bp & 31);
     buf <<= skip;
     nb -= skip;
+    if (nb <= 32) refill();
   }
   __device__ __forceinline__ void refill() {
-    while (nb <= 56) {
-      const uint64_t b = byte < nbytes ? p[byte] : 0;
-      buf |= b << (56 - nb);
-      nb += 8;
-      byte++;
+    while (nb <= 32) {
+      const uint32_t x = wi < nw ? word(wi) : 0u;
+      buf |= (uint64_t)x << (32 - nb);
+      nb += 32;
+      wi++;
     }
   }
+  // top L (<= 64) bits, also when L exceeds the buffered bits
+  __device__ __forceinline__ uint64_t peek(int L) const {
+    if (L <= nb) return buf >> (64 - L);
+    const uint64_t x = wi < nw ? word(wi) : 0u;
+    return (buf | (x >> (nb - 32))) >> (64 - L);
+  }
   __device__ __forceinline__ void consume(int L) {
-    buf = L >= 64 ? 0 : buf << L;
-    nb -= L;
-    if (nb <= 56) refill();
+    if (L < nb) {
+      buf <<= L;
+      nb -= L;
+    } else {  // L >= nb: drop the buffer and skip the rest of L in the next word
+      const int skip = L - nb;
+      buf = 0;
+      nb = 0;
+      refill();
+      buf <<= skip;
+      nb -= skip;
+    }
+    if (nb <= 32) refill();
   }
 };
 
@@ -1444,7 +1478,7 @@ __device__ long long hd_decode(const HDTables& T, const HDShared* S, const uint8
       sym = -1;
       for (L = K + 1; L <= T.maxlen; L++) {
         if (!T.count[L]) continue;
-        const unsigned long long c = br.buf >> (64 - L);
+        const unsigned long long c = br.peek(L);
         if (c >= T.first_code[L] && c - T.first_code[L] < (unsigned long long)T.count[L]) {
           sym = T.syms[T.first_rank[L] + (int)(c - T.first_code[L])];
           break;
