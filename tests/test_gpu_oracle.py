@@ -73,3 +73,32 @@ def test_thin_field_whole_block_tuner(oracle, dims):
             assert e[c] == errs[level - 1, i]
     for mode in ("cr", "tp"):
         assert hb.compress(f, hb.ErrorBoundSpec("rel", 1e-3), mode) == oracle.compress(vals, "rel", 1e-3, mode, 3)
+
+
+# every interpolation config per level on shapes with many interior blocks:
+# exercises the TMA dependency passes (k_pass.cu) for all four stencil /
+# scheme combinations, all seq1d axis orders, even and odd E rows (direct vs
+# gathered class-0 lattice), f32 and f64
+CFG_SHAPES = [
+    ((70, 90, 100), "f32"),   # seq1d order z, y, x; even E rows
+    ((100, 66, 97), "f32"),   # order x, z, y; odd E rows -> gathered lattice
+    ((48, 120, 40), "f64"),   # order y, x, z
+]
+CFGS = [bytes([0, 0, 0, 0]), bytes([1, 1, 1, 1]), bytes([2, 2, 2, 2]), bytes([3, 3, 3, 3]), bytes([2, 1, 3, 0])]
+
+
+@pytest.mark.parametrize("dims,dt", CFG_SHAPES)
+def test_forced_configs_match_oracle(oracle, dims, dt):
+    vals = synth.make("grf", dims, seed=21, dtype=dt)
+    f = hb.Field(vals)
+    eb = oracle.resolve_eb(vals, "rel", 1e-3)
+    for cb in CFGS:
+        cfg = hb.InterpConfig.from_bytes(cb)
+        qf = hb.decompose(f, eb, cfg)
+        codes, oidx, oval, anchors = oracle.decompose(vals, eb, list(cb))
+        assert np.array_equal(qf.codes.reshape(-1), codes.reshape(-1)), (dims, cb)
+        assert np.array_equal(qf.outlier_indices, oidx), (dims, cb)
+        assert np.array_equal(qf.outlier_values, oval), (dims, cb)
+        rec = hb.reconstruct(qf, eb, cfg, dims=f.dims, ndim=f.ndim)
+        ref = oracle.reconstruct(codes, oidx, oval, anchors, eb, list(cb), dims, vals.dtype)
+        assert np.array_equal(rec.values.reshape(-1), ref.reshape(-1)), (dims, cb)
