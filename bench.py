@@ -299,7 +299,10 @@ def run_ours(args):
             pass
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 2), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic, "algo_bytes": int(ab), "ms": round(ms, 4),
-                "peak_kind": peak_kind}
+                "peak_kind": peak_kind,
+                # DRAM bytes actually moved (ncu, profiles/traffic.json) over the same time: the level
+                # passes trade f64 class round trips through HBM for halo recompute
+                "traffic_gbs": round(traffic / (ms / 1e3) / 1e9, 1) if traffic else None}
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
