@@ -1092,7 +1092,7 @@ void launch_bit_encode(const uint8_t* in, const unsigned long long* n_dev, int w
 // frequent symbol has the 1-bit code "0" (smooth fields) runs of zero bits
 // are consumed with one clz.  Output goes out in aligned 16-byte stores.
 
-constexpr int HD_S = 1024;       // bits per subsequence
+constexpr int HD_S = 512;        // bits per subsequence
 constexpr int HD_K = 12;         // LUT bits
 constexpr int HD_PASSES = 4;
 
