@@ -396,7 +396,43 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 3D f64 array (n0, n1, n2) with rows of n2p doubles; box for an axis-`a` source
+// Encoded maps are cached per thread: a context reuses its arena, so from the
+// second call on every launch finds its maps here instead of re-encoding
+// ~20 per level on the critical path between the tuner read-back and the
+// level launches.
+struct MapKey {
+  const double* base;
+  long long n0, n1, n2, n2p;
+  int a;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && n0 == o.n0 && n1 == o.n1 && n2 == o.n2 && n2p == o.n2p && a == o.a;
+  }
+};
+struct MapCache {
+  static constexpr int CAP = 256;
+  MapKey key[CAP];
+  alignas(64) CUtensorMap map[CAP];
+  int n = 0, next = 0;
+};
+
+bool encode_map(CUtensorMap* m, const double* base, long long n0, long long n1, long long n2, long long n2p, int a);
+
 bool make_map(CUtensorMap* m, const double* base, long long n0, long long n1, long long n2, long long n2p, int a) {
+  static thread_local MapCache* cache = new MapCache();
+  const MapKey k{base, n0, n1, n2, n2p, a};
+  for (int i = 0; i < cache->n; i++)
+    if (cache->key[i] == k) {
+      *m = cache->map[i];
+      return true;
+    }
+  if (!encode_map(m, base, n0, n1, n2, n2p, a)) return false;
+  const int slot = cache->n < MapCache::CAP ? cache->n++ : (cache->next++ % MapCache::CAP);
+  cache->key[slot] = k;
+  cache->map[slot] = *m;
+  return true;
+}
+
+bool encode_map(CUtensorMap* m, const double* base, long long n0, long long n1, long long n2, long long n2p, int a) {
   auto fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dim[3] = {(cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)n0};
