@@ -20,7 +20,7 @@
 
 namespace hb {
 
-constexpr int TUNE_THREADS = 256;
+constexpr int TUNE_THREADS = 512;
 // CONFIG_CHOICES (tuning.py:29) as InterpConfig bytes: bit0 linear, bit1 seq1d
 __constant__ uint8_t c_choice[4] = {0x0, 0x2, 0x1, 0x3};
 
