@@ -35,11 +35,17 @@ namespace hb {
 
 namespace {
 
-constexpr int TX = 8, TY = 8, TZ = 32;
+constexpr int TY = 8, TZ = 32;
 constexpr int TZH = TZ + 4;  // z-source box z0-2 .. z0+TZ+1 (even start, 16-byte multiple)
 constexpr int T_THREADS = TY * 32;
-constexpr int SLOT = (TX + 3) * TY * TZ;  // doubles per source tile slot (largest box)
-static_assert(TX * TY * TZH <= SLOT && TX * (TY + 3) * TZ <= SLOT, "slot too small");
+// targets per thread along x (per step: 16 was measured slower for every K on
+// B200 -- fewer resident blocks outweigh the amortised per-thread setup)
+constexpr __host__ __device__ int txof(int) { return 8; }
+// doubles per source tile slot: the largest of the x / y / z boxes
+constexpr __host__ __device__ int cmax(int a, int b) { return a > b ? a : b; }
+constexpr __host__ __device__ int slot_of(int tx) {
+  return cmax((tx + 3) * TY * TZ, cmax(tx * (TY + 3) * TZ, tx * TY * TZH));
+}
 
 struct alignas(64) TMaps {
   CUtensorMap m[6];
@@ -138,7 +144,7 @@ __device__ __forceinline__ Tile tile_of(int a) {
 }
 
 // One thread: targets (x0 + i, y, z), i < nx.  INT: every stencil complete.
-template <typename T, bool DEC, int K, bool LINEAR, bool INT, bool LV1>
+template <typename T, bool DEC, int K, bool LINEAR, bool INT, bool LV1, int TX = txof(K)>
 __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, int CLS, int AXM, int x0, int nx,
                                        int y, int z, int yl, int zl, long long lin, long long slot, const T* o,
                                        const uint8_t* cd, double eb, double two_eb, double inv_two_eb,
@@ -168,7 +174,7 @@ __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, 
       m &= m - 1;
       const Tile t = tile_of(a);
       sax[j] = a;
-      tb[j] = tiles + j * SLOT + yl * t.sy + zl + (a == 2);  // z box starts one below the first tap
+      tb[j] = tiles + j * slot_of(TX) + yl * t.sy + zl + (a == 2);  // z box starts one below the first tap
       tsx[j] = t.sx;
       tst[j] = t.st;
       scls[j] = (INT || a == 0) ? (LINEAR ? ST_MID : ST_CUBIC) : classify(a == 1 ? P1 : P2, g.D[a], 1, LINEAR);
@@ -236,7 +242,7 @@ __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, 
   }
 }
 
-template <typename T, bool DEC, int K, bool LINEAR, bool LV1>
+template <typename T, bool DEC, int K, bool LINEAR, bool LV1, int TX = txof(K)>
 __global__ void __launch_bounds__(T_THREADS, 2) k_tpass(const __grid_constant__ TPassArgs A,
                                                          const __grid_constant__ TMaps M) {
   extern __shared__ __align__(128) double tiles[];
@@ -283,7 +289,7 @@ __global__ void __launch_bounds__(T_THREADS, 2) k_tpass(const __grid_constant__ 
       m &= m - 1;
       const CUtensorMap* map = &M.m[A.map[k][j]];
       // the innermost start coordinate must be 16-byte aligned: the z box starts at z0 - 2
-      tma_load_3d(tiles + j * SLOT, map, z0 - 2 * (a == 2), y0 - (a == 1), x0 - (a == 0), &bar);
+      tma_load_3d(tiles + j * slot_of(TX), map, z0 - 2 * (a == 2), y0 - (a == 1), x0 - (a == 0), &bar);
     }
   }
   // originals / codes of this thread's run, in flight with the boxes
@@ -403,9 +409,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 struct MapKey {
   const double* base;
   long long n0, n1, n2, n2p;
-  int a;
+  int a, tx;
   bool operator==(const MapKey& o) const {
-    return base == o.base && n0 == o.n0 && n1 == o.n1 && n2 == o.n2 && n2p == o.n2p && a == o.a;
+    return base == o.base && n0 == o.n0 && n1 == o.n1 && n2 == o.n2 && n2p == o.n2p && a == o.a && tx == o.tx;
   }
 };
 struct MapCache {
@@ -415,30 +421,33 @@ struct MapCache {
   int n = 0, next = 0;
 };
 
-bool encode_map(CUtensorMap* m, const double* base, long long n0, long long n1, long long n2, long long n2p, int a);
+bool encode_map(CUtensorMap* m, const double* base, long long n0, long long n1, long long n2, long long n2p, int a,
+                int tx);
 
-bool make_map(CUtensorMap* m, const double* base, long long n0, long long n1, long long n2, long long n2p, int a) {
+bool make_map(CUtensorMap* m, const double* base, long long n0, long long n1, long long n2, long long n2p, int a,
+              int tx) {
   static thread_local MapCache* cache = new MapCache();
-  const MapKey k{base, n0, n1, n2, n2p, a};
+  const MapKey k{base, n0, n1, n2, n2p, a, tx};
   for (int i = 0; i < cache->n; i++)
     if (cache->key[i] == k) {
       *m = cache->map[i];
       return true;
     }
-  if (!encode_map(m, base, n0, n1, n2, n2p, a)) return false;
+  if (!encode_map(m, base, n0, n1, n2, n2p, a, tx)) return false;
   const int slot = cache->n < MapCache::CAP ? cache->n++ : (cache->next++ % MapCache::CAP);
   cache->key[slot] = k;
   cache->map[slot] = *m;
   return true;
 }
 
-bool encode_map(CUtensorMap* m, const double* base, long long n0, long long n1, long long n2, long long n2p, int a) {
+bool encode_map(CUtensorMap* m, const double* base, long long n0, long long n1, long long n2, long long n2p, int a,
+                int tx) {
   auto fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dim[3] = {(cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)n0};
   const cuuint64_t str[2] = {(cuuint64_t)(n2p * 8), (cuuint64_t)(n1 * n2p * 8)};
   const cuuint32_t box[3] = {(cuuint32_t)(a == 2 ? TZH : TZ), (cuuint32_t)(a == 1 ? TY + 3 : TY),
-                             (cuuint32_t)(a == 0 ? TX + 3 : TX)};
+                             (cuuint32_t)(a == 0 ? tx + 3 : tx)};
   const cuuint32_t es[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dim, str, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -453,7 +462,7 @@ struct Launch {
 };
 
 // map of class `cn` (0 = E) used as an axis-`a` source; reuses an identical one
-int map_for(Launch& L, int cn, int a, int keys[6]) {
+int map_for(Launch& L, int cn, int a, int tx, int keys[6]) {
   const int key = cn * 4 + a;
   for (int i = 0; i < L.nmaps; i++)
     if (keys[i] == key) return i;
@@ -463,11 +472,11 @@ int map_for(Launch& L, int cn, int a, int keys[6]) {
   for (int b = 0; b < 3; b++) n[b] = ((cn >> b) & 1) ? g.D[b] >> 1 : (g.D[b] + 1) >> 1;
   bool ok;
   if (cn == 0 && !L.gathered)
-    ok = make_map(&L.M.m[L.nmaps], L.A.E, g.Ed[0], g.Ed[1], g.Ed[2], g.Ed[2], a);
+    ok = make_map(&L.M.m[L.nmaps], L.A.E, g.Ed[0], g.Ed[1], g.Ed[2], g.Ed[2], a, tx);
   else if (cn == 0)
-    ok = make_map(&L.M.m[L.nmaps], L.A.scr + 6 * L.A.cstride, n[0], n[1], n[2], (n[2] + 1) & ~1ll, a);
+    ok = make_map(&L.M.m[L.nmaps], L.A.scr + 6 * L.A.cstride, n[0], n[1], n[2], (n[2] + 1) & ~1ll, a, tx);
   else
-    ok = make_map(&L.M.m[L.nmaps], L.A.scr + (cn - 1) * L.A.cstride, n[0], n[1], n[2], (n[2] + 1) & ~1ll, a);
+    ok = make_map(&L.M.m[L.nmaps], L.A.scr + (cn - 1) * L.A.cstride, n[0], n[1], n[2], (n[2] + 1) & ~1ll, a, tx);
   if (!ok) return -1;
   keys[L.nmaps] = key;
   return L.nmaps++;
@@ -480,18 +489,19 @@ bool plan_step(Launch& L, int K, const int* cls, const int* axm, int n) {
   L.nmaps = 0;
   int keys[6] = {-1, -1, -1, -1, -1, -1};
   long long mx = 0;
+  const int tx = txof(K);
   for (int k = 0; k < n; k++) {
     A.cls[k] = cls[k];
     A.axm[k] = axm[k];
     long long nd[3];
     for (int a = 0; a < 3; a++) nd[a] = ((cls[k] >> a) & 1) ? A.g.D[a] >> 1 : (A.g.D[a] + 1) >> 1;
     if (!nd[0] || !nd[1] || !nd[2]) return false;
-    mx = std::max(mx, (nd[0] + TX - 1) / TX);
+    mx = std::max(mx, (nd[0] + tx - 1) / tx);
     int m = axm[k];
     for (int j = 0; j < K; j++) {
       const int a = __builtin_ctz(m);
       m &= m - 1;
-      const int idx = map_for(L, cls[k] & ~(1 << a), a, keys);
+      const int idx = map_for(L, cls[k] & ~(1 << a), a, tx, keys);
       if (idx < 0) return false;
       A.map[k][j] = idx;
     }
@@ -510,11 +520,11 @@ void launch_step(const Launch& L, cudaStream_t s, int* launches) {
     mz = std::max(mz, (n2 + TZ - 1) / TZ);
     my = std::max(my, (n1 + TY - 1) / TY);
   }
-  const size_t smem = (size_t)K * SLOT * 8;
+  const size_t smem = (size_t)K * slot_of(txof(K)) * 8;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute((const void*)k_tpass<T, DEC, K, LINEAR, LV1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(3 * SLOT * 8));
+                         (int)smem);
     attr = true;
   }
   const dim3 grid((unsigned)mz, (unsigned)my, (unsigned)(A.nbx * A.ncls));
