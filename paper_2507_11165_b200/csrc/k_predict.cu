@@ -106,33 +106,45 @@ void make_level_geom(const uint64_t dims[3], int level, LevelGeom* g) {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_minmax(const T* __restrict__ v, unsigned long long n, DevState* st) {
-  double lo = INFINITY, hi = -INFINITY;
+  // min / max in the field's own type (exact), widened once at the end; a
+  // value is non-finite iff its exponent field is all ones
+  T lo = (T)INFINITY, hi = (T)-INFINITY;
   bool bad = false;
-  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x * 4;
-  for (unsigned long long i = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
-    T x[4];
-    if (i + 4 <= n && sizeof(T) == 4) {
-      float4 f = *reinterpret_cast<const float4*>(v + i);
-      x[0] = (T)f.x, x[1] = (T)f.y, x[2] = (T)f.z, x[3] = (T)f.w;
+  constexpr int V = 32 / sizeof(T);  // elements per thread per step (two 16-byte loads)
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x * V;
+  for (unsigned long long i = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) * V; i < n; i += stride) {
+    T x[V];
+    if (i + V <= n) {
+      const uint4* p = reinterpret_cast<const uint4*>(v + i);
+      const uint4 a = __ldcs(p), b = __ldcs(p + 1);
+      const uint4 ab[2] = {a, b};
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+        memcpy(x + h * (V / 2), &ab[h], 16);
     } else {
-      for (int k = 0; k < 4; k++) x[k] = i + k < n ? v[i + k] : v[i];
+      for (int k = 0; k < V; k++) x[k] = i + k < n ? v[i + k] : v[i];
     }
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-      double d = (double)x[k];
-      bad |= !isfinite(d);
-      lo = fmin(lo, d);
-      hi = fmax(hi, d);
+    for (int k = 0; k < V; k++) {
+      if (sizeof(T) == 4) {
+        bad |= (__float_as_uint((float)x[k]) & 0x7f800000u) == 0x7f800000u;
+      } else {
+        bad |= (((unsigned long long)__double_as_longlong((double)x[k])) & 0x7ff0000000000000ull) ==
+               0x7ff0000000000000ull;
+      }
+      lo = x[k] < lo ? x[k] : lo;
+      hi = x[k] > hi ? x[k] : hi;
     }
   }
+  double dlo = (double)lo, dhi = (double)hi;
   for (int o = 16; o > 0; o >>= 1) {
-    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    dlo = fmin(dlo, __shfl_xor_sync(0xffffffffu, dlo, o));
+    dhi = fmax(dhi, __shfl_xor_sync(0xffffffffu, dhi, o));
   }
   bad = __any_sync(0xffffffffu, bad);
   if ((threadIdx.x & 31) == 0) {
-    atomicMin(&st->vmin_bits, ord_bits(lo));
-    atomicMax(&st->vmax_bits, ord_bits(hi));
+    atomicMin(&st->vmin_bits, ord_bits(dlo));
+    atomicMax(&st->vmax_bits, ord_bits(dhi));
     if (bad) raise_flag(st, F_NONFINITE);
   }
 }
@@ -167,8 +179,8 @@ void launch_minmax(const void* field, int prec, unsigned long long n, DevState* 
   if (eb_mode == 1) {
     k_minmax_init<<<1, 1, 0, s>>>(st);
     (*launches)++;
-    unsigned long long blocks = cdiv(n, 256ull * 4);
-    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    unsigned long long blocks = cdiv(n, 256ull * (32 / prec));
+    if (blocks > 148ull * 8) blocks = 148ull * 8;
     if (prec == 4)
       k_minmax<float><<<(unsigned)blocks, 256, 0, s>>>((const float*)field, n, st);
     else
