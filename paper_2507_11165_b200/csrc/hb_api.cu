@@ -21,8 +21,28 @@ using namespace hb;
 
 
 
+// A launch sequence recorded as a CUDA graph: replayed when a call repeats
+// the previous call's parameters exactly (same buffers, shape, header and
+// tuned config), so the ~40 launches of a compress tail or a decompress go
+// out as one graph launch instead of one host launch each.
+struct GraphSlot {
+  std::vector<uint8_t> key;
+  int seen = 0;
+  cudaGraphExec_t exec = nullptr;
+  int nl = 0;
+  int nev = 0;                      // profiling marks after the sequence (host bookkeeping
+  std::vector<const char*> names;   // of the event-record nodes the graph contains)
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
+    seen = 0;
+    key.clear();
+  }
+};
+
 struct hb_ctx {
   int device = 0;
+  GraphSlot g_comp, g_dec;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   uint8_t* arena = nullptr;
@@ -46,7 +66,14 @@ struct hb_ctx {
       ev.push_back(e);
       ev_name.push_back(nullptr);
     }
-    cudaEventRecord(ev[nev], stream);
+    // inside a stream capture the record must be external to become an
+    // event-record node of the graph (the flag is invalid outside a capture)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(stream, &cs);
+    if (cs == cudaStreamCaptureStatusActive)
+      cudaEventRecordWithFlags(ev[nev], stream, cudaEventRecordExternal);
+    else
+      cudaEventRecord(ev[nev], stream);
     ev_name[nev] = name;
     nev++;
   }
@@ -156,6 +183,70 @@ MemKind mem_kind(const void* p) {
     return MEM_HOST;
   }
   return (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) ? MEM_DEVICE : MEM_HOST;
+}
+
+// key builder: raw bytes of every host value a recorded sequence depends on
+struct KeyBuf {
+  std::vector<uint8_t> b;
+  template <class T>
+  KeyBuf& add(const T& v) {
+    const uint8_t* p = reinterpret_cast<const uint8_t*>(&v);
+    b.insert(b.end(), p, p + sizeof(T));
+    return *this;
+  }
+  KeyBuf& add_bytes(const void* p, size_t n) {
+    b.insert(b.end(), (const uint8_t*)p, (const uint8_t*)p + n);
+    return *this;
+  }
+};
+
+// Enqueue directly, or through the slot's graph: a key seen on two calls in a
+// row is captured once (stream capture of the very same enqueue code) and
+// replayed from then on.  HB_NO_GRAPHS=1 disables it.
+template <class F>
+int run_graphed(hb_ctx* ctx, GraphSlot& gs, const std::vector<uint8_t>& key, int* nl, F&& enqueue) {
+  static const bool off = getenv("HB_NO_GRAPHS") != nullptr;
+  if (off) return enqueue();
+  const cudaStream_t s = ctx->stream;
+  if (gs.exec && gs.key == key) {
+    const cudaError_t e = cudaGraphLaunch(gs.exec, s);
+    if (e != cudaSuccess) return set_err(ctx, HB_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(e));
+    *nl += gs.nl;
+    ctx->nev = gs.nev;
+    for (int i = 0; i < gs.nev; i++) ctx->ev_name[i] = gs.names[i];
+    return HB_OK;
+  }
+  if (gs.key == key) {
+    gs.seen++;
+  } else {
+    gs.reset();
+    gs.key = key;
+    gs.seen = 1;
+  }
+  if (gs.seen < 2) return enqueue();
+  const int nl0 = *nl;
+  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return enqueue();  // capture unavailable (e.g. legacy stream): run directly
+  const int rc = enqueue();
+  cudaGraph_t g = nullptr;
+  e = cudaStreamEndCapture(s, &g);
+  if (rc || e != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    gs.reset();
+    return rc ? rc : set_err(ctx, HB_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(e));
+  }
+  e = cudaGraphInstantiate(&gs.exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    gs.exec = nullptr;
+    gs.reset();
+    return set_err(ctx, HB_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e));
+  }
+  gs.nl = *nl - nl0;
+  gs.nev = ctx->nev;
+  gs.names.assign(ctx->ev_name.begin(), ctx->ev_name.begin() + ctx->nev);
+  e = cudaGraphLaunch(gs.exec, s);
+  return e == cudaSuccess ? HB_OK : set_err(ctx, HB_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(e));
 }
 
 // bump allocator over the context arena
@@ -379,6 +470,10 @@ struct Hdr46 {
   uint8_t b[46];
 };
 
+__global__ void k_put_hdr46(uint8_t* dst, Hdr46 h) {
+  if (threadIdx.x < 46) dst[threadIdx.x] = h.b[threadIdx.x];
+}
+
 int validate_field_args(hb_ctx* ctx, int precision, const uint64_t dims[3], int ndim) {
   if (precision != 4 && precision != 8) return set_err(ctx, HB_EFIELD, "unsupported precision %d", precision);
   if (ndim != 2 && ndim != 3) return set_err(ctx, HB_EFIELD, "ndim must be 2 or 3, got %d", ndim);
@@ -434,6 +529,8 @@ void hb_ctx_destroy(hb_ctx* ctx) {
   if (ctx->arena) cudaFree(ctx->arena);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (auto e : ctx->ev) cudaEventDestroy(e);
+  ctx->g_comp.reset();
+  ctx->g_dec.reset();
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -634,58 +731,69 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
     memcpy(hcfg, pc, 4);
   }
   if (!tune_only) {
-    // 3) anchors + the level walk with fused quantize / reorder / histogram
-    const unsigned long long abase = 46 + 8;
-    launch_anchor_init(dfield, prec, dims, A, E, seq, arch + abase, st, true, s, &nl);
-    static const char* lvl_names[5] = {"", "level1", "level2", "level3", "level4"};
-    for (int level = top; level >= 1; level--) {
-      LevelGeom g;
-      make_level_geom(dims, level, &g);
-      launch_level_compress(g, dfield, prec, E, seq, obm, st, s, &nl, hcfg[level - 1] & 3,
-                            reinterpret_cast<double*>(base + o_scr));
-      ctx->mark(lvl_names[level]);
-    }
-    // 4) outliers straight into the archive (archive.py:65-71)
-    const unsigned long long obase = abase + na * prec + 8;
-    launch_outlier_compact(obm, N, dfield, prec, arch + obase, nullptr, nullptr, lb, st, s, &nl);
-    launch_stream_offset(obase, prec, st, s, &nl);
-    k_set_u64<<<1, 1, 0, s>>>(&st->seq_len, N);
-    nl++;
-    ctx->mark("outliers");
-    unsigned long long* lbx = lb + lb_oc;
-    // 5) lossless pipeline, final record assembled in place at the stream offset
-    if (mode == 0) {
-      launch_huffman_build(st, N, hf, s, &nl);
-      ctx->mark("huff_build");
-      launch_huffman_encode(seq, N, hf, lbx, st, s, &nl);
-      ctx->mark("huff_encode");
-      lbx += lb_he;
-      launch_reduce_chain_impl(2, 4, SRC_MEM, hf, &st->hf_rec_len, 0, cb1.max_words, cb1.rb, &st->bm[0], rre4,
-                               nullptr, &st->scratch[1], lbx, lb_c1, cb1.table, s, &nl);
-      lbx += 4 * lb_c1;
-      launch_reduce_chain_impl(3, 1, SRC_TCMS, rre4, &st->scratch[1], 8, cb2.max_words, cb2.rb, &st->bm[1], arch,
-                               &st->scratch[0], &st->stream_len, lbx, lb_c2, cb2.table, s, &nl);
-    } else {
-      lbx += lb_he;
-      launch_reduce_chain_impl(2, 1, SRC_TP, seq, &st->seq_len, 0, cb1.max_words, cb1.rb, &st->bm[2], arch,
-                               &st->scratch[0], &st->stream_len, lbx, lb_c1, cb1.table, s, &nl);
-    }
-    // 6) escape decision, header, counts (archive.py:55-74)
-    Hdr46 h;
-    memset(&h, 0, sizeof h);
-    memcpy(h.b, "CSZH", 4);
-    h.b[4] = 1;
-    h.b[5] = (uint8_t)mode;
-    h.b[6] = (uint8_t)prec;
-    h.b[7] = (uint8_t)ndim;
-    h.b[8] = (uint8_t)A;
-    for (int a = 0; a < 3; a++)
-      for (int i = 0; i < 8; i++) h.b[14 + 8 * a + i] = (uint8_t)(dims[a] >> (8 * i));
-    uint8_t* d_h = reinterpret_cast<uint8_t*>(&st->scratch[8]);  // 46 bytes inside DevState scratch
-    if ((rc = up.put(d_h, h.b, 46, s))) return rc;
-    ctx->mark("lossless");
-    launch_archive_tail_impl(arch, obase, prec, seq, N, d_h, na, st, s, &nl);
-    ctx->mark("archive");
+    // 3)-6): everything after the tuner depends only on the buffers, the
+    // shape and the tuned config, so it is one (graph-replayable) sequence
+    auto tail = [&]() -> int {
+      // 3) anchors + the level walk with fused quantize / reorder / histogram
+      const unsigned long long abase = 46 + 8;
+      launch_anchor_init(dfield, prec, dims, A, E, seq, arch + abase, st, true, s, &nl);
+      static const char* lvl_names[5] = {"", "level1", "level2", "level3", "level4"};
+      for (int level = top; level >= 1; level--) {
+        LevelGeom g;
+        make_level_geom(dims, level, &g);
+        launch_level_compress(g, dfield, prec, E, seq, obm, st, s, &nl, hcfg[level - 1] & 3,
+                              reinterpret_cast<double*>(base + o_scr));
+        ctx->mark(lvl_names[level]);
+      }
+      // 4) outliers straight into the archive (archive.py:65-71)
+      const unsigned long long obase = abase + na * prec + 8;
+      launch_outlier_compact(obm, N, dfield, prec, arch + obase, nullptr, nullptr, lb, st, s, &nl);
+      launch_stream_offset(obase, prec, st, s, &nl);
+      k_set_u64<<<1, 1, 0, s>>>(&st->seq_len, N);
+      nl++;
+      ctx->mark("outliers");
+      unsigned long long* lbx = lb + lb_oc;
+      // 5) lossless pipeline, final record assembled in place at the stream offset
+      if (mode == 0) {
+        launch_huffman_build(st, N, hf, s, &nl);
+        ctx->mark("huff_build");
+        launch_huffman_encode(seq, N, hf, lbx, st, s, &nl);
+        ctx->mark("huff_encode");
+        lbx += lb_he;
+        launch_reduce_chain_impl(2, 4, SRC_MEM, hf, &st->hf_rec_len, 0, cb1.max_words, cb1.rb, &st->bm[0], rre4,
+                                 nullptr, &st->scratch[1], lbx, lb_c1, cb1.table, s, &nl);
+        lbx += 4 * lb_c1;
+        launch_reduce_chain_impl(3, 1, SRC_TCMS, rre4, &st->scratch[1], 8, cb2.max_words, cb2.rb, &st->bm[1], arch,
+                                 &st->scratch[0], &st->stream_len, lbx, lb_c2, cb2.table, s, &nl);
+      } else {
+        lbx += lb_he;
+        launch_reduce_chain_impl(2, 1, SRC_TP, seq, &st->seq_len, 0, cb1.max_words, cb1.rb, &st->bm[2], arch,
+                                 &st->scratch[0], &st->stream_len, lbx, lb_c1, cb1.table, s, &nl);
+      }
+      // 6) escape decision, header, counts (archive.py:55-74)
+      Hdr46 h;
+      memset(&h, 0, sizeof h);
+      memcpy(h.b, "CSZH", 4);
+      h.b[4] = 1;
+      h.b[5] = (uint8_t)mode;
+      h.b[6] = (uint8_t)prec;
+      h.b[7] = (uint8_t)ndim;
+      h.b[8] = (uint8_t)A;
+      for (int a = 0; a < 3; a++)
+        for (int i = 0; i < 8; i++) h.b[14 + 8 * a + i] = (uint8_t)(dims[a] >> (8 * i));
+      uint8_t* d_h = reinterpret_cast<uint8_t*>(&st->scratch[8]);  // 46 bytes inside DevState scratch
+      k_put_hdr46<<<1, 64, 0, s>>>(d_h, h);  // a kernel parameter, not a pinned upload: replay-safe
+      nl++;
+      ctx->mark("lossless");
+      launch_archive_tail_impl(arch, obase, prec, seq, N, d_h, na, st, s, &nl);
+      ctx->mark("archive");
+      return HB_OK;
+    };
+    KeyBuf kb;
+    kb.add(dfield).add(prec).add_bytes(dims, 3 * sizeof(uint64_t)).add(ndim).add(mode).add(ctx->arena);
+    kb.add(ctx->arena_size).add_bytes(hcfg, 4).add(ctx->prof);
+    rc = run_graphed(ctx, ctx->g_comp, kb.b, &nl, tail);
+    if (rc) return rc;
   }
   ctx->launches = nl;
   HostStatus hs;
@@ -804,67 +912,81 @@ int hb_decompress(hb_ctx* ctx, const void* archive, size_t len, void* field_out,
   unsigned long long* lb = reinterpret_cast<unsigned long long*>(base + o_lb);
   int nl = 0;
   if (host_arch) CU(cudaMemcpyAsync(base + o_arch, archive, len, cudaMemcpyHostToDevice, s));
-  CU(cudaMemsetAsync(st, 0, sizeof(DevState), s));
-  CU(cudaMemsetAsync(lb, 0, lbn * 8 * 12, s));
-  CU(cudaMemsetAsync(base + o_hd, 0, hd_bytes, s));
-  ctx->nev = 0;
-  ctx->mark("start");
-  k_set_cfg_eb<<<1, 1, 0, s>>>(st, I.cfg[0], I.cfg[1], I.cfg[2], I.cfg[3], I.eb);
-  nl++;
-  k_set_u64<<<1, 1, 0, s>>>(&st->scratch[2], I.stream_len);
-  nl++;
-  k_set_u64<<<1, 1, 0, s>>>(&st->scratch[3], I.outlier_count);
-  nl++;
-  // outliers (archive.py:136-150)
-  if (I.outlier_count) {
-    launch_outliers_parse(arch + I.outlier_off, prec, I.outlier_count, &st->scratch[3], N, oidx, oval, st, s, &nl);
-  }
-  // code stream -> level-grouped sequence (archive.py:157-164)
-  const uint8_t* stream = arch + I.stream_off;
-  const uint8_t* codes = seq;
-  unsigned long long* lbx = lb;
-  if (I.escape) {
-    if (I.stream_len != N) return set_err(ctx, HB_EARCHIVE, "decoded code sequence has %llu bytes, expected %llu",
-                                          (unsigned long long)I.stream_len, N);
-    codes = stream;
-    launch_count_zeros(stream, N, st, s, &nl);
-  } else if (I.mode == 0) {
-    // CR: huffman <- rre <- tcms <- rze (stages.py:426-427)
-    launch_reduce_decode_impl(3, stream, &st->scratch[2], cap_rec, ta, &st->scratch[4], tmp, base + o_bmd, lbx, lbn,
-                              st, s, &nl);
-    lbx += 4 * lbn;
-    launch_tcms_decode(ta, &st->scratch[4], cap_rec, tb, &st->scratch[5], st, s, &nl);
-    launch_reduce_decode_impl(2, tb, &st->scratch[5], cap_rec, tc, &st->scratch[6], tmp, base + o_bmd, lbx, lbn, st,
-                              s, &nl);
-    lbx += 4 * lbn;
-    ctx->mark("decode_bitmaps");
-    launch_huffman_decode_impl(tc, &st->scratch[6], N, N, cap_rec, seq, base + o_hd, lbx, st, s, &nl);
-  } else {
-    // TP: tcms <- bit <- rre (stages.py:434-435)
-    launch_reduce_decode_impl(2, stream, &st->scratch[2], cap_rec, ta, &st->scratch[4], tmp, base + o_bmd, lbx, lbn,
-                              st, s, &nl);
-    lbx += 4 * lbn;
-    launch_bit_decode(ta, &st->scratch[4], tb, &st->scratch[5], cap_rec, st, s, &nl);
-    launch_tcms_decode(tb, &st->scratch[5], cap_rec, seq, &st->scratch[6], st, s, &nl);
-    k_check_len<<<1, 1, 0, s>>>(&st->scratch[6], N, st, F_ARCHIVE);
+  // everything from here on depends only on the buffers and the header: one
+  // (graph-replayable when the archive and output live on the device) sequence
+  auto seq_all = [&]() -> int {
+    CU(cudaMemsetAsync(st, 0, sizeof(DevState), s));
+    CU(cudaMemsetAsync(lb, 0, lbn * 8 * 12, s));
+    CU(cudaMemsetAsync(base + o_hd, 0, hd_bytes, s));
+    ctx->nev = 0;
+    ctx->mark("start");
+    k_set_cfg_eb<<<1, 1, 0, s>>>(st, I.cfg[0], I.cfg[1], I.cfg[2], I.cfg[3], I.eb);
     nl++;
-    launch_count_zeros(seq, N, st, s, &nl);
-  }
-  ctx->mark("decode_stream");
-  // reconstruct (predictor.py:378-416) with fused inverse reorder
-  if (top == 0) {
-    launch_copy_anchors_out(arch + I.anchor_off, prec, N, out, st, s, &nl);
-  } else {
-    launch_anchor_load(arch + I.anchor_off, prec, I.dims, A, E, s, &nl);
-    for (int level = top; level >= 1; level--) {
-      LevelGeom g;
-      make_level_geom(I.dims, level, &g);
-      launch_level_decompress(g, codes, oidx, oval, &st->scratch[3], E, out, prec, st, s, &nl, I.cfg[level - 1] & 3,
-                              reinterpret_cast<double*>(base + o_scr));
-      static const char* dl_names[5] = {"", "rlevel1", "rlevel2", "rlevel3", "rlevel4"};
-      ctx->mark(dl_names[level]);
+    k_set_u64<<<1, 1, 0, s>>>(&st->scratch[2], I.stream_len);
+    nl++;
+    k_set_u64<<<1, 1, 0, s>>>(&st->scratch[3], I.outlier_count);
+    nl++;
+    // outliers (archive.py:136-150)
+    if (I.outlier_count) {
+      launch_outliers_parse(arch + I.outlier_off, prec, I.outlier_count, &st->scratch[3], N, oidx, oval, st, s, &nl);
     }
+    // code stream -> level-grouped sequence (archive.py:157-164)
+    const uint8_t* stream = arch + I.stream_off;
+    const uint8_t* codes = seq;
+    unsigned long long* lbx = lb;
+    if (I.escape) {
+      if (I.stream_len != N) return set_err(ctx, HB_EARCHIVE, "decoded code sequence has %llu bytes, expected %llu",
+                                            (unsigned long long)I.stream_len, N);
+      codes = stream;
+      launch_count_zeros(stream, N, st, s, &nl);
+    } else if (I.mode == 0) {
+      // CR: huffman <- rre <- tcms <- rze (stages.py:426-427)
+      launch_reduce_decode_impl(3, stream, &st->scratch[2], cap_rec, ta, &st->scratch[4], tmp, base + o_bmd, lbx, lbn,
+                                st, s, &nl);
+      lbx += 4 * lbn;
+      launch_tcms_decode(ta, &st->scratch[4], cap_rec, tb, &st->scratch[5], st, s, &nl);
+      launch_reduce_decode_impl(2, tb, &st->scratch[5], cap_rec, tc, &st->scratch[6], tmp, base + o_bmd, lbx, lbn, st,
+                                s, &nl);
+      lbx += 4 * lbn;
+      ctx->mark("decode_bitmaps");
+      launch_huffman_decode_impl(tc, &st->scratch[6], N, N, cap_rec, seq, base + o_hd, lbx, st, s, &nl);
+    } else {
+      // TP: tcms <- bit <- rre (stages.py:434-435)
+      launch_reduce_decode_impl(2, stream, &st->scratch[2], cap_rec, ta, &st->scratch[4], tmp, base + o_bmd, lbx, lbn,
+                                st, s, &nl);
+      lbx += 4 * lbn;
+      launch_bit_decode(ta, &st->scratch[4], tb, &st->scratch[5], cap_rec, st, s, &nl);
+      launch_tcms_decode(tb, &st->scratch[5], cap_rec, seq, &st->scratch[6], st, s, &nl);
+      k_check_len<<<1, 1, 0, s>>>(&st->scratch[6], N, st, F_ARCHIVE);
+      nl++;
+      launch_count_zeros(seq, N, st, s, &nl);
+    }
+    ctx->mark("decode_stream");
+    // reconstruct (predictor.py:378-416) with fused inverse reorder
+    if (top == 0) {
+      launch_copy_anchors_out(arch + I.anchor_off, prec, N, out, st, s, &nl);
+    } else {
+      launch_anchor_load(arch + I.anchor_off, prec, I.dims, A, E, s, &nl);
+      for (int level = top; level >= 1; level--) {
+        LevelGeom g;
+        make_level_geom(I.dims, level, &g);
+        launch_level_decompress(g, codes, oidx, oval, &st->scratch[3], E, out, prec, st, s, &nl, I.cfg[level - 1] & 3,
+                                reinterpret_cast<double*>(base + o_scr));
+        static const char* dl_names[5] = {"", "rlevel1", "rlevel2", "rlevel3", "rlevel4"};
+        ctx->mark(dl_names[level]);
+      }
+    }
+    return HB_OK;
+  };
+  if (host_arch || o_out) {
+    rc = seq_all();
+  } else {
+    KeyBuf kb;
+    kb.add(archive).add(len).add(field_out).add(cap).add(ctx->arena).add(ctx->arena_size).add(ctx->prof);
+    kb.add_bytes(&I, sizeof I);
+    rc = run_graphed(ctx, ctx->g_dec, kb.b, &nl, seq_all);
   }
+  if (rc) return rc;
   ctx->launches = nl;
   HostStatus hs;
   rc = read_status(ctx, st, &hs);
