@@ -856,10 +856,26 @@ int hb_decompress(hb_ctx* ctx, const void* archive, size_t len, void* field_out,
     rc = parse_info((const uint8_t*)archive, len, &I, ctx);
   } else {
     // header fields live in device memory: fetch the few bytes the walk needs
+    // through the pinned buffer (async copy + stream sync); the first read
+    // brings the header and the anchor count (bytes [0, 54)) in one trip
+    if ((rc = ensure_pinned(ctx, 1 << 16))) return rc;
+    uint8_t* pin = ctx->pinned + 4096 + 1024;
+    size_t have = 0;
     rc = parse_info_t(
         [&](size_t off, size_t n, uint8_t* dst) -> int {
-          cudaError_t e = cudaMemcpy(dst, (const uint8_t*)archive + off, n, cudaMemcpyDeviceToHost);
-          return e == cudaSuccess ? 0 : set_err(ctx, HB_ECUDA, "cudaMemcpy: %s", cudaGetErrorString(e));
+          if (off + n <= have) {
+            memcpy(dst, pin + off, n);
+            return 0;
+          }
+          const bool head = off == 0;
+          const size_t m = head ? std::min<size_t>(len, 64) : n;
+          cudaError_t e = cudaMemcpyAsync(head ? pin : pin + 512, (const uint8_t*)archive + off, m,
+                                          cudaMemcpyDeviceToHost, ctx->stream);
+          if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+          if (e != cudaSuccess) return set_err(ctx, HB_ECUDA, "header read: %s", cudaGetErrorString(e));
+          if (head) have = m;
+          memcpy(dst, head ? pin : pin + 512, n);
+          return 0;
         },
         len, &I, ctx);
   }
