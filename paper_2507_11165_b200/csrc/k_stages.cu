@@ -677,6 +677,45 @@ __global__ void __launch_bounds__(256) k_huff_encode(const uint8_t* __restrict__
     // OR only the non-zero bits: the all-zero canonical code (the most
     // frequent symbol) just advances the bit position
     unsigned long long pos = in_smem ? shift0 + excl : tstart + excl;
+    if (in_smem && nb <= 128) {
+      // common case: the thread's whole bit string fits 128 bits -- build it
+      // in registers (branch-free shifts) and OR it in as <= 5 aligned words
+      uint64_t ah = 0, al = 0;
+#pragma unroll
+      for (int k = 0; k < HE_SYMS; k++) {
+        const unsigned long long e = k < cnt ? stab[(w[k >> 2] >> (8 * (k & 3))) & 0xFF] : 0ull;
+        const int L = (int)(e >> 56);
+        const uint64_t c = e & ((1ull << 56) - 1);
+        if (L) {
+          ah = (ah << L) | (al >> (64 - L));
+          al = (al << L) | c;
+        }
+      }
+      if (nb) {
+        // left-align to 128 bits, then shift right by the in-word bit offset
+        const int sh = 128 - (int)nb;
+        uint64_t H, Lo;
+        if (sh >= 64) {
+          H = al << (sh - 64);
+          Lo = 0;
+        } else if (sh > 0) {
+          H = (ah << sh) | (al >> (64 - sh));
+          Lo = al << sh;
+        } else {
+          H = ah;
+          Lo = al;
+        }
+        const int b = (int)(pos & 31);
+        const uint64_t T0 = H >> b, T1 = b ? (H << (64 - b)) | (Lo >> b) : Lo, T2 = b ? Lo << (64 - b) : 0ull;
+        const uint32_t wd[5] = {(uint32_t)(T0 >> 32), (uint32_t)T0, (uint32_t)(T1 >> 32), (uint32_t)T1,
+                                (uint32_t)(T2 >> 32)};
+        const unsigned long long wi0 = pos >> 5;
+        const int nwd = (b + (int)nb + 31) >> 5;
+#pragma unroll
+        for (int q = 0; q < 5; q++)
+          if (q < nwd && wd[q]) atomicOr(&hbuf[wi0 + q], wd[q]);
+      }
+    } else
 #pragma unroll
     for (int k = 0; k < HE_SYMS; k++) {
       const unsigned long long e = k < cnt ? stab[(w[k >> 2] >> (8 * (k & 3))) & 0xFF] : 0ull;
