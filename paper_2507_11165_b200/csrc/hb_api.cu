@@ -43,6 +43,7 @@ struct GraphSlot {
 struct hb_ctx {
   int device = 0;
   GraphSlot g_comp, g_dec;
+  cudaEvent_t enter_ev = nullptr;  // orders an own stream after the legacy default stream
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   uint8_t* arena = nullptr;
@@ -268,6 +269,17 @@ int ensure_arena(hb_ctx* ctx, size_t need) {
   CU(cudaMalloc(&ctx->arena, sz));
   ctx->arena_size = sz;
   return 0;
+}
+
+// entry of every call that touches the device: select the device and, for a
+// context on its own stream, wait for work already queued on the legacy
+// default stream (the inputs a default-stream caller just produced)
+void ctx_enter(hb_ctx* ctx) {
+  cudaSetDevice(ctx->device);
+  if (ctx->own_stream && ctx->enter_ev) {
+    cudaEventRecord(ctx->enter_ev, cudaStreamLegacy);
+    cudaStreamWaitEvent(ctx->stream, ctx->enter_ev, 0);
+  }
 }
 
 int ensure_pinned(hb_ctx* ctx, size_t need) {
@@ -513,6 +525,11 @@ int hb_ctx_create(int device, void* cuda_stream, hb_ctx** out) {
       return HB_ECUDA;
     }
     ctx->own_stream = true;
+    // a caller without a stream of its own (torch's default stream, plain
+    // CUDA code) produced its inputs on the legacy default stream, which a
+    // non-blocking stream does not wait for: every call orders the context's
+    // stream after it (ctx_enter)
+    cudaEventCreateWithFlags(&ctx->enter_ev, cudaEventDisableTiming);
   }
   if (ensure_pinned(ctx, 1 << 16)) {
     delete ctx;
@@ -531,6 +548,7 @@ void hb_ctx_destroy(hb_ctx* ctx) {
   for (auto e : ctx->ev) cudaEventDestroy(e);
   ctx->g_comp.reset();
   ctx->g_dec.reset();
+  if (ctx->enter_ev) cudaEventDestroy(ctx->enter_ev);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -565,7 +583,7 @@ int hb_compress_bound(const uint64_t dims[3], int precision, size_t* max_bytes) 
 int hb_value_range(hb_ctx* ctx, const void* field, int prec, uint64_t n, double* vmin, double* vmax) {
   if (!ctx || !field || !vmin || !vmax || n == 0) return ctx ? set_err(ctx, HB_EARG, "bad argument") : HB_EARG;
   if (prec != 4 && prec != 8) return set_err(ctx, HB_EFIELD, "unsupported precision %d", prec);
-  cudaSetDevice(ctx->device);
+  ctx_enter(ctx);
   const cudaStream_t s = ctx->stream;
   Layout L;
   const size_t o_st = L.take(sizeof(DevState));
@@ -615,7 +633,7 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
   if (mode != 0 && mode != 1) return set_err(ctx, HB_EARG, "mode must be 'cr' or 'tp'");
   if (eb_mode != 0 && eb_mode != 1) return set_err(ctx, HB_EBOUND, "error-bound mode must be 'abs' or 'rel'");
   if (!(isfinite(mag) && mag > 0)) return set_err(ctx, HB_EBOUND, "error-bound magnitude must be positive, got %g", mag);
-  cudaSetDevice(ctx->device);
+  ctx_enter(ctx);
   const cudaStream_t s = ctx->stream;
   const unsigned long long N = dims[0] * dims[1] * dims[2];
   const int A = anchor_stride(dims), top = ilog2i(A);
@@ -847,7 +865,7 @@ int hb_tune(hb_ctx* ctx, const void* field, int precision, const uint64_t dims[3
 
 int hb_decompress(hb_ctx* ctx, const void* archive, size_t len, void* field_out, size_t cap, hb_info* info_out) {
   if (!ctx || !archive || !field_out) return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
-  cudaSetDevice(ctx->device);
+  ctx_enter(ctx);
   const cudaStream_t s = ctx->stream;
   const bool host_arch = mem_kind(archive) == MEM_HOST;
   hb_info I;
@@ -1030,7 +1048,7 @@ int hb_decompose(hb_ctx* ctx, const void* field, int prec, const uint64_t dims[3
   int rc = validate_field_args(ctx, prec, dims, dims[2] == 1 ? 2 : 3);
   if (rc) return rc;
   if (!(isfinite(eb) && eb > 0)) return set_err(ctx, HB_EBOUND, "error bound must be positive and finite, got %g", eb);
-  cudaSetDevice(ctx->device);
+  ctx_enter(ctx);
   const cudaStream_t s = ctx->stream;
   const unsigned long long N = dims[0] * dims[1] * dims[2];
   const int A = anchor_stride(dims), top = ilog2i(A);
@@ -1096,7 +1114,7 @@ int hb_reconstruct(hb_ctx* ctx, const uint8_t* seq_in, const uint64_t* oidx_in, 
     return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
   if (!(isfinite(eb) && eb > 0)) return set_err(ctx, HB_EBOUND, "error bound must be positive and finite, got %g", eb);
   if (stride < 1 || stride > 16 || (stride & (stride - 1))) return set_err(ctx, HB_EARG, "bad stride");
-  cudaSetDevice(ctx->device);
+  ctx_enter(ctx);
   const cudaStream_t s = ctx->stream;
   const unsigned long long N = dims[0] * dims[1] * dims[2];
   const int A = stride, top = ilog2i(A);
@@ -1173,7 +1191,7 @@ int hb_reconstruct(hb_ctx* ctx, const uint8_t* seq_in, const uint64_t* oidx_in, 
 
 int hb_reorder(hb_ctx* ctx, const uint8_t* codes, const uint64_t dims[3], int stride, uint8_t* seq_out) {
   if (!ctx || !codes || !dims || !seq_out) return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
-  cudaSetDevice(ctx->device);
+  ctx_enter(ctx);
   const unsigned long long N = dims[0] * dims[1] * dims[2];
   Layout L;
   const size_t o_in = L.take(N + 64), o_out = L.take(N + 64);
@@ -1190,7 +1208,7 @@ int hb_reorder(hb_ctx* ctx, const uint8_t* codes, const uint64_t dims[3], int st
 
 int hb_inverse_reorder(hb_ctx* ctx, const uint8_t* seq, const uint64_t dims[3], int stride, uint8_t* codes_out) {
   if (!ctx || !seq || !dims || !codes_out) return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
-  cudaSetDevice(ctx->device);
+  ctx_enter(ctx);
   const unsigned long long N = dims[0] * dims[1] * dims[2];
   Layout L;
   const size_t o_in = L.take(N + 64), o_out = L.take(N + 64);
@@ -1212,7 +1230,7 @@ int hb_stage_encode(hb_ctx* ctx, int stage, int width, const void* in, size_t n,
   if (stage != HB_PIPE_CR && stage != HB_PIPE_TP && stage != HB_STAGE_HUFFMAN && width != 1 && width != 2 &&
       width != 4 && width != 8)
     return set_err(ctx, HB_ESTAGE, "symbol width must be one of (1, 2, 4, 8), got %d", width);
-  cudaSetDevice(ctx->device);
+  ctx_enter(ctx);
   const cudaStream_t s = ctx->stream;
   Layout L;
   const size_t o_st = L.take(sizeof(DevState));
@@ -1304,7 +1322,7 @@ int hb_stage_encode(hb_ctx* ctx, int stage, int width, const void* in, size_t n,
 
 int hb_stage_decode(hb_ctx* ctx, int stage, const void* in, size_t n, void* out, size_t cap, size_t* out_len) {
   if (!ctx || (!in && n) || !out) return ctx ? set_err(ctx, HB_EARG, "null argument") : HB_EARG;
-  cudaSetDevice(ctx->device);
+  ctx_enter(ctx);
   const cudaStream_t s = ctx->stream;
   Layout L;
   const size_t o_st = L.take(sizeof(DevState));
