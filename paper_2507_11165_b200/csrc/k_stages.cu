@@ -1701,9 +1701,90 @@ __global__ void __launch_bounds__(256) k_hd_emit(const uint8_t* rec, const HDTab
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) raise_flag(st, F_STAGE, 162);
 }
 
+// In-place fix-up, iterated to convergence inside one cooperative launch:
+// every round re-decodes the subsequences whose start disagrees with their
+// predecessor's end (the first round from the first pass's codeword starts
+// via the 64-bit sync window), then a grid-wide barrier.  A stale read of a
+// predecessor's end only delays a fix by one round; each round fixes at least
+// the first inconsistent subsequence, so the loop terminates.  Replaces a
+// fixed number of passes + a serial sweep (that sweep cost 0.36 s on a rough
+// 512^3 field whose corrections cascade over many subsequences).
+constexpr int HD_ROUNDS = 1000;  // then the serial sweep (adversarial streams only)
+
+__device__ __forceinline__ void hd_grid_barrier(unsigned* count, volatile unsigned* gen, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == nblocks - 1) {
+      *count = 0;
+      __threadfence();
+      atomicAdd(const_cast<unsigned*>(gen), 1u);
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_hd_fix(const uint8_t* rec, const HDTables* T, HDWork W) {
+  __shared__ HDShared S;
+  __shared__ int s_any;
+  if (!T->ok) return;  // uniform: every block returns
+  hd_load_shared(&S, T);
+  __syncthreads();
+  const unsigned long long nsub = T->nsub;
+  const uint8_t* pay = rec + T->pay_off;
+  unsigned* bar = reinterpret_cast<unsigned*>(W.changed + HD_ROUNDS + 2);
+  volatile unsigned long long* E = W.e[0];
+  for (int p = 1; p <= HD_ROUNDS; p++) {
+    bool ch = false;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nsub;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+      const unsigned long long want = i == 0 ? 0ull : E[i - 1];
+      const unsigned long long s0 = W.s[0][i];
+      if (want == s0 || want == ~0ull) continue;
+      unsigned long long e = want;
+      long long c = 0;
+      bool done = false;
+      if (s0 == i * HD_S && E[i] != ~0ull && want >= i * HD_S) {
+        // still the first pass's decode: run from the true start until it
+        // meets one of its codeword starts (from there both are identical)
+        unsigned long long ps;
+        const unsigned long long bm = W.bmask[i];
+        const long long k = hd_decode<false, false, true>(*T, &S, pay, want, (i + 1) * HD_S, &ps, nullptr, nullptr,
+                                                          i * HD_S, bm);
+        if (k >= 0) {
+          const unsigned long long q = ps - i * HD_S;
+          const unsigned before = __popcll(bm & ((1ull << q) - 1));
+          W.c[0][i] = W.c[0][i] - before + (unsigned)k;
+          W.s[0][i] = want;
+          done = true;
+        }
+      }
+      if (!done) {
+        if (want < (i + 1) * HD_S) c = hd_decode<false>(*T, &S, pay, want, (i + 1) * HD_S, &e, nullptr);
+        W.c[0][i] = c < 0 ? 0u : (unsigned)c;
+        W.s[0][i] = want;
+        __threadfence();
+        E[i] = c < 0 ? ~0ull : e;
+      }
+      ch = true;
+    }
+    if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(&W.changed[p], 1);
+    hd_grid_barrier(bar, bar + 1, gridDim.x);
+    if (threadIdx.x == 0) s_any = *(volatile int*)&W.changed[p];
+    __syncthreads();
+    if (!s_any) return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) W.changed[HD_ROUNDS + 1] = 1;  // not converged: serial sweep
+}
+
 // serial fallback when HD_PASSES did not converge (adversarial streams)
 __global__ void k_hd_serial(const uint8_t* rec, const HDTables* T, HDWork W, int fin) {
-  if (!T->ok || !W.changed[HD_PASSES]) return;
+  if (!T->ok || !W.changed[HD_ROUNDS + 1]) return;
   const unsigned long long nsub = T->nsub;
   const uint8_t* pay = rec + T->pay_off;
   for (unsigned long long i = 1; i < nsub; i++) {
@@ -1725,7 +1806,7 @@ __global__ void k_hd_serial(const uint8_t* rec, const HDTables* T, HDWork W, int
 
 size_t huffman_decode_ws_bytes(unsigned long long max_payload_bytes) {
   const unsigned long long nsub = cdiv(max_payload_bytes * 8, HD_S) + 1;
-  return sizeof(HDTables) + 256 + nsub * (8 * 2 + 8 * 2 + 4 * 2 + 8 + 8) + 64 + 256;
+  return sizeof(HDTables) + 256 + nsub * (8 * 2 + 8 * 2 + 4 * 2 + 8 + 8) + 64 + 256 + (HD_ROUNDS + 8) * 4;
 }
 
 void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long* len_dev, unsigned long long n,
@@ -1750,17 +1831,32 @@ void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long*
     W.c[b] = reinterpret_cast<unsigned*>(p);
     p += nsub_max * 4;
   }
-  W.changed = reinterpret_cast<int*>(p);  // HD_PASSES + 1 ints, zeroed by the caller
+  W.changed = reinterpret_cast<int*>(p);  // HD_ROUNDS + 4 ints (flags, barrier), zeroed by the caller
   k_hd_setup<<<1, 256, 0, s>>>(hf_rec, len_dev, n, max_out, T, st);
   (*launches)++;
   const unsigned g = persist_grid(cdiv(nsub_max, 256));
   k_hd_first<<<g, 256, 0, s>>>(hf_rec, T, W, st);
   (*launches)++;
-  for (int pss = 1; pss <= HD_PASSES; pss++) {
-    k_hd_pass<<<g, 256, 0, s>>>(pss, hf_rec, T, W);
+  {  // every block resident (cooperative launch): the fix-up rounds use a grid barrier
+    static int per_sm = 0;
+    if (!per_sm) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hd_fix, 256, 0);
+      if (per_sm < 1) per_sm = 1;
+    }
+    const unsigned gf = (unsigned)std::min<unsigned long long>(cdiv(nsub_max, 256), (unsigned long long)kSMs * per_sm);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gf);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_hd_fix, hf_rec, (const HDTables*)T, W);
     (*launches)++;
   }
-  const int fin = HD_PASSES & 1;
+  const int fin = 0;
   k_hd_serial<<<1, 1, 0, s>>>(hf_rec, T, W, fin);
   (*launches)++;
   k_hd_scan<<<persist_grid(cdiv(nsub_max, 8192)), 256, 0, s>>>(T, W, fin, lb_ws, st);
