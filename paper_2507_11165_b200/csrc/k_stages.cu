@@ -12,6 +12,10 @@
 #include <cuda_runtime.h>
 #include <stdio.h>
 
+#include <vector>
+#include <cstdio>
+#include <cstdlib>
+
 #include "hb_common.cuh"
 #include "hb_kernels.h"
 
@@ -1563,6 +1567,7 @@ __global__ void __launch_bounds__(256) k_hd_first(const uint8_t* rec, const HDTa
     W.bmask[i] = m;
     W.s[0][i] = s0;
     W.e[0][i] = c < 0 ? ~0ull : e;  // error end never matches a successor start
+    W.e[1][i] = W.e[0][i];          // first-pass ends, read-only during the fix-up's first round
     W.c[0][i] = c < 0 ? 0u : (unsigned)c;
   }
 }
@@ -1731,7 +1736,7 @@ __device__ __forceinline__ void hd_grid_barrier(unsigned* count, volatile unsign
 
 __global__ void __launch_bounds__(256) k_hd_fix(const uint8_t* rec, const HDTables* T, HDWork W) {
   __shared__ HDShared S;
-  __shared__ int s_any;
+  __shared__ int s_n;
   if (!T->ok) return;  // uniform: every block returns
   hd_load_shared(&S, T);
   __syncthreads();
@@ -1739,45 +1744,90 @@ __global__ void __launch_bounds__(256) k_hd_fix(const uint8_t* rec, const HDTabl
   const uint8_t* pay = rec + T->pay_off;
   unsigned* bar = reinterpret_cast<unsigned*>(W.changed + HD_ROUNDS + 2);
   volatile unsigned long long* E = W.e[0];
-  for (int p = 1; p <= HD_ROUNDS; p++) {
-    bool ch = false;
+  // full decode of subsequence i from the predecessor's end
+  auto redecode = [&](unsigned long long i, unsigned long long want) {
+    unsigned long long e = want;
+    long long c = 0;
+    if (want < (i + 1) * HD_S) c = hd_decode<false>(*T, &S, pay, want, (i + 1) * HD_S, &e, nullptr);
+    W.c[0][i] = c < 0 ? 0u : (unsigned)c;
+    W.s[0][i] = want;
+    __threadfence();
+    E[i] = c < 0 ? ~0ull : e;
+  };
+  // round 1: every subsequence against the first pass; from the true start
+  // until it meets one of the first pass's codeword starts (64-bit window)
+  // (predecessor ends are read from the first pass's copy: no thread sees a
+  // half-updated neighbour, so every subsequence whose predecessor
+  // resynchronised comes out exact)
+  const unsigned long long* E1 = W.e[1];
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nsub;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long want = i == 0 ? 0ull : E1[i - 1];
+    const unsigned long long s0 = W.s[0][i];
+    if (want == s0 || want == ~0ull) continue;
+    bool done = false;
+    if (E1[i] != ~0ull && want >= i * HD_S) {
+      unsigned long long ps;
+      const unsigned long long bm = W.bmask[i];
+      const long long k = hd_decode<false, false, true>(*T, &S, pay, want, (i + 1) * HD_S, &ps, nullptr, nullptr,
+                                                        i * HD_S, bm);
+      if (k >= 0) {
+        const unsigned long long q = ps - i * HD_S;
+        const unsigned before = __popcll(bm & ((1ull << q) - 1));
+        W.c[0][i] = W.c[0][i] - before + (unsigned)k;
+        W.s[0][i] = want;
+        done = true;
+      }
+    }
+    if (!done) redecode(i, want);
+  }
+  // later rounds: runs of still inconsistent subsequences are chains (the
+  // first pass did not resynchronise before their end, e.g. inside periodic
+  // stretches); one thread per chain head walks it sequentially until the
+  // stored state agrees again or it reaches the next head (its own walker)
+  unsigned long long* wl = W.off;     // work list (the scan's offsets are written later)
+  unsigned long long* mark = W.s[1];  // round that listed the subsequence
+  for (int r = 2; r <= HD_ROUNDS; r++) {
+    hd_grid_barrier(bar, bar + 1, gridDim.x);
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nsub;
          i += (unsigned long long)gridDim.x * blockDim.x) {
+      // list chain heads only: inconsistent, with a consistent predecessor
       const unsigned long long want = i == 0 ? 0ull : E[i - 1];
-      const unsigned long long s0 = W.s[0][i];
-      if (want == s0 || want == ~0ull) continue;
-      unsigned long long e = want;
-      long long c = 0;
-      bool done = false;
-      if (s0 == i * HD_S && E[i] != ~0ull && want >= i * HD_S) {
-        // still the first pass's decode: run from the true start until it
-        // meets one of its codeword starts (from there both are identical)
-        unsigned long long ps;
-        const unsigned long long bm = W.bmask[i];
-        const long long k = hd_decode<false, false, true>(*T, &S, pay, want, (i + 1) * HD_S, &ps, nullptr, nullptr,
-                                                          i * HD_S, bm);
-        if (k >= 0) {
-          const unsigned long long q = ps - i * HD_S;
-          const unsigned before = __popcll(bm & ((1ull << q) - 1));
-          W.c[0][i] = W.c[0][i] - before + (unsigned)k;
-          W.s[0][i] = want;
-          done = true;
-        }
+      const bool bad_i = want != ~0ull && want != W.s[0][i];
+      bool bad_prev = false;
+      if (i > 0) {
+        const unsigned long long wp = i == 1 ? 0ull : E[i - 2];
+        bad_prev = wp != ~0ull && wp != W.s[0][i - 1];
       }
-      if (!done) {
-        if (want < (i + 1) * HD_S) c = hd_decode<false>(*T, &S, pay, want, (i + 1) * HD_S, &e, nullptr);
-        W.c[0][i] = c < 0 ? 0u : (unsigned)c;
-        W.s[0][i] = want;
-        __threadfence();
-        E[i] = c < 0 ? ~0ull : e;
+      if (bad_i && !bad_prev) {
+        const int k = atomicAdd(&W.changed[r], 1);
+        wl[k] = i;
+        mark[i] = (unsigned long long)r;
       }
-      ch = true;
     }
-    if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(&W.changed[p], 1);
     hd_grid_barrier(bar, bar + 1, gridDim.x);
-    if (threadIdx.x == 0) s_any = *(volatile int*)&W.changed[p];
+    if (threadIdx.x == 0) s_n = *(volatile int*)&W.changed[r];
     __syncthreads();
-    if (!s_any) return;
+    const int n = s_n;
+    if (n == 0) return;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+      // a chain may alternate: an entry that agrees with its (new)
+      // predecessor can still have moved its own end in round 1, so the walk
+      // goes on while the current or the next entry disagrees
+      auto bad = [&](unsigned long long j) {
+        const unsigned long long want = j == 0 ? 0ull : E[j - 1];
+        return want != ~0ull && want != W.s[0][j];
+      };
+      unsigned long long i = wl[k];
+      for (;;) {
+        if (bad(i))
+          redecode(i, i == 0 ? 0ull : E[i - 1]);
+        else if (i + 1 >= nsub || !bad(i + 1))
+          break;
+        i++;
+        if (i >= nsub || mark[i] == (unsigned long long)r) break;
+      }
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) W.changed[HD_ROUNDS + 1] = 1;  // not converged: serial sweep
 }
@@ -1855,6 +1905,19 @@ void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long*
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, k_hd_fix, hf_rec, (const HDTables*)T, W);
     (*launches)++;
+    if (getenv("HB_DEBUG_HD")) {
+      std::vector<int> ch(HD_ROUNDS + 4);
+      cudaStreamSynchronize(s);
+      cudaMemcpy(ch.data(), W.changed, ch.size() * 4, cudaMemcpyDeviceToHost);
+      int rounds = 1;
+      for (int i = 2; i <= HD_ROUNDS; i++) rounds += ch[i] != 0;
+      unsigned long long nsub = 0;
+      cudaMemcpy(&nsub, &T->nsub, 8, cudaMemcpyDeviceToHost);
+      fprintf(stderr, "hd_fix: grid %u nsub %llu rounds-with-changes %d serial %d; per round:", gf, nsub, rounds,
+              ch[HD_ROUNDS + 1]);
+      for (int i = 2; i <= rounds + 1 && i <= 40; i++) fprintf(stderr, " %d", ch[i]);
+      fprintf(stderr, "\n");
+    }
   }
   const int fin = 0;
   k_hd_serial<<<1, 1, 0, s>>>(hf_rec, T, W, fin);
