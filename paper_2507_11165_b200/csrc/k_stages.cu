@@ -1007,6 +1007,18 @@ __global__ void k_tcms_decode(const uint8_t* rec, const unsigned long long* len_
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *out_len = orig;
   const unsigned long long nw = body / w;
+  if (w == 1 && (reinterpret_cast<uintptr_t>(out) & 7) == 0) {
+    // 8 bytes per thread: one aligned 8-byte store, SWAR un-zigzag
+    const unsigned long long n8 = nw / 8;
+    const uint8_t* q = rec + 10;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+      *reinterpret_cast<uint64_t*>(out + 8 * i) = unzz8x1(ld_bytes(q + 8 * i, 8));
+    for (unsigned long long i = n8 * 8 + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nw;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+      out[i] = (uint8_t)unzz(q[i], 1);
+    return;
+  }
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nw;
        i += (unsigned long long)gridDim.x * blockDim.x)
     st_bytes(out + i * w, unzz(ld_bytes(rec + 10 + i * w, w), w), w);
@@ -1038,6 +1050,19 @@ __global__ void k_bit_decode(const uint8_t* rec, const unsigned long long* len_d
   const int nb = 8 * w;
   const unsigned long long nwords = body / w;
   const uint8_t* q = rec + 10;
+  if (w == 1 && (reinterpret_cast<uintptr_t>(out) & 7) == 0) {
+    // one 8-byte tile per thread: its 8 plane bytes in, all 8 words out
+    const unsigned long long nt = nwords / 8;
+    for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < nt;
+         t += (unsigned long long)gridDim.x * blockDim.x) {
+      const uint64_t g = ld_bytes(q + 8 * t, 8);
+      uint64_t u = 0;
+#pragma unroll
+      for (int j = 0; j < 8; j++) u |= (uint64_t)bit_plane(g, j) << (8 * j);
+      *reinterpret_cast<uint64_t*>(out + 8 * t) = u;
+    }
+    return;
+  }
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nwords;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned long long t = i / nb;
@@ -1931,9 +1956,19 @@ void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long*
 // zero count over a sequence (escape / TP paths)
 __global__ void k_count_zeros(const uint8_t* seq, unsigned long long n, DevState* st) {
   unsigned c = 0;
+  // aligned 16-byte body, per-byte compare in SIMD-within-a-register
+  const unsigned long long head = min(n, (unsigned long long)((16 - (reinterpret_cast<uintptr_t>(seq) & 15)) & 15));
+  const unsigned long long n16 = (n - head) / 16;
+  const uint4* v = reinterpret_cast<const uint4*>(seq + head);
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint4 x = __ldcs(v + i);
+    c += (__popc(__vcmpeq4(x.x, 0u)) + __popc(__vcmpeq4(x.y, 0u)) + __popc(__vcmpeq4(x.z, 0u)) +
+          __popc(__vcmpeq4(x.w, 0u))) >> 3;
+  }
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x)
-    c += seq[i] == 0;
+    if (i < head || i >= head + 16 * n16) c += seq[i] == 0;
   c = warp_sum<unsigned>(c);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(&st->zero_count, (unsigned long long)c);
 }
