@@ -1498,7 +1498,10 @@ __device__ long long hd_decode(const HDTables& T, const HDShared* S, const uint8
       }
     }
     if (MASK && pos - start < 64) m |= 1ull << (pos - start);
-    if (rs >= 0 && !(br.buf >> 63)) {  // run of the 1-bit code "0"
+    // run of the 1-bit code "0": long runs in one step; short ones go through
+    // the multi-symbol table below (up to 4 codewords per lookup)
+    if (rs >= 0 && !(br.buf >> 63) &&
+        (SYNC || (MASK && pos - start < 64) || (br.buf >> 56) == 0)) {
       unsigned long long z = br.buf ? (unsigned long long)__clzll(br.buf) : 64ull;
       if (z > (unsigned long long)br.nb) z = br.nb;
       if (z > lim - pos) z = lim - pos;
