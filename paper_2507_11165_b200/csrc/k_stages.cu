@@ -1442,6 +1442,24 @@ struct OutWriter {
     p++;
     if (!(p & 15)) flush_chunk(p - 16, 16);
   }
+  // n (<= 4) packed bytes, first in the low byte, in one or two shifts
+  __device__ __forceinline__ void put4(uint32_t pk, int n) {
+    const uint64_t v = n >= 4 ? (uint64_t)pk : ((uint64_t)pk & ((1ull << (8 * n)) - 1));
+    const int k = (int)(p & 15);
+    const int e = k + n;  // window bytes [k, e)
+    if (k < 8) {
+      lo |= v << (8 * k);
+      if (e > 8) hi |= v >> (64 - 8 * k);  // k > 4 here, shift < 64
+    } else {
+      hi |= v << (8 * (k - 8));
+    }
+    p += n;
+    if (e >= 16) {
+      // window complete: flush, then carry the bytes that spilled past byte 15
+      flush_chunk(p - e, 16);
+      if (e > 16) lo = v >> (8 * (16 - k));
+    }
+  }
   // n copies of byte b: masked fill of the current 16-byte window, whole
   // windows as single 16-byte stores
   __device__ __forceinline__ void run(int b, unsigned long long n) {
@@ -1528,11 +1546,10 @@ __device__ long long hd_decode(const HDTables& T, const HDShared* S, const uint8
       if (n >= 2 && pos + b <= lim) {
         if (EMIT) {
           const uint32_t pk = S->msym[key];
-          for (int q = 0; q < n; q++) {
-            const int sy = (pk >> (8 * q)) & 0xFF;
-            ow->put(sy);
-            ow->zeros += sy == 0;
-          }
+          ow->put4(pk, n);
+          // zero symbols among the n packed bytes
+          const uint32_t live = n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1);
+          ow->zeros += (unsigned)__popc(__vcmpeq4(pk, 0u) & live) >> 3;
         }
         pos += b;
         cnt += n;
