@@ -242,7 +242,10 @@ __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, 
   }
 }
 
-template <typename T, bool DEC, int K, bool LINEAR, bool LV1, int TX = txof(K)>
+// CLSC >= 0: the launch holds the single class CLSC interpolated along all
+// its odd axes (multidim), known at compile time -- every parity test, tap
+// stride and slot term folds; CLSC < 0: classes and axes from the arguments
+template <typename T, bool DEC, int K, bool LINEAR, bool LV1, int CLSC = -1, int TX = txof(K)>
 __global__ void __launch_bounds__(T_THREADS, 2) k_tpass(const __grid_constant__ TPassArgs A,
                                                          const __grid_constant__ TMaps M) {
   extern __shared__ __align__(128) double tiles[];
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(T_THREADS, 2) k_tpass(const __grid_constant__ 
   // the source tiles they share (and the halo rows of their neighbours)
   // are still in L2 when the second reader comes
   const int bx = (int)blockIdx.z / A.ncls, k = (int)blockIdx.z - bx * A.ncls;
-  const int CLS = A.cls[k], AXM = A.axm[k];
+  const int CLS = CLSC >= 0 ? CLSC : A.cls[k], AXM = CLSC >= 0 ? CLSC : A.axm[k];
   const int n0 = cdim1(g, CLS, 0), n1 = cdim1(g, CLS, 1), n2 = cdim1(g, CLS, 2);
   const int x0 = bx * TX, y0 = blockIdx.y * TY, z0 = blockIdx.x * TZ;
   if (x0 >= n0 || y0 >= n1 || z0 >= n2) return;  // block past this class's extent (uniform)
@@ -510,7 +513,7 @@ bool plan_step(Launch& L, int K, const int* cls, const int* axm, int n) {
   return true;
 }
 
-template <typename T, bool DEC, int K, bool LINEAR, bool LV1>
+template <typename T, bool DEC, int K, bool LINEAR, bool LV1, int CLSC = -1>
 void launch_step(const Launch& L, cudaStream_t s, int* launches) {
   const TPassArgs& A = L.A;
   long long mz = 0, my = 0;
@@ -523,12 +526,12 @@ void launch_step(const Launch& L, cudaStream_t s, int* launches) {
   const size_t smem = (size_t)K * slot_of(txof(K)) * 8;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute((const void*)k_tpass<T, DEC, K, LINEAR, LV1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute((const void*)k_tpass<T, DEC, K, LINEAR, LV1, CLSC>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   const dim3 grid((unsigned)mz, (unsigned)my, (unsigned)(A.nbx * A.ncls));
-  k_tpass<T, DEC, K, LINEAR, LV1><<<grid, T_THREADS, smem, s>>>(A, L.M);
+  k_tpass<T, DEC, K, LINEAR, LV1, CLSC><<<grid, T_THREADS, smem, s>>>(A, L.M);
   (*launches)++;
 }
 
@@ -536,16 +539,30 @@ void launch_step(const Launch& L, cudaStream_t s, int* launches) {
 // is launched, so a shape TMA cannot express falls back cleanly
 template <typename T, bool DEC, bool LINEAR, bool LV1>
 bool run_passes(const Launch& base, int cfg, cudaStream_t s, int* launches) {
-  Launch L[3] = {base, base, base};
+  Launch L[7] = {base, base, base, base, base, base, base};
   int K[3];
-  if ((cfg & 2) == 0) {  // multidim: a class interpolates along all its odd axes
+  if ((cfg & 2) == 0 && !LV1) {  // multidim, small levels: one launch per dependency step
     const int c1[3] = {1, 2, 4}, c2[3] = {3, 5, 6}, c3[1] = {7};
-    K[0] = 1, K[1] = 2, K[2] = 3;
     if (!plan_step(L[0], 1, c1, c1, 3) || !plan_step(L[1], 2, c2, c2, 3) || !plan_step(L[2], 3, c3, c3, 1))
       return false;
     launch_step<T, DEC, 1, LINEAR, LV1>(L[0], s, launches);
     launch_step<T, DEC, 2, LINEAR, LV1>(L[1], s, launches);
     launch_step<T, DEC, 3, LINEAR, LV1>(L[2], s, launches);
+    return true;
+  }
+  if ((cfg & 2) == 0) {  // multidim, level 1: one launch per class (class and axes compile-time)
+    const int order[7] = {1, 2, 4, 3, 5, 6, 7};
+    for (int q = 0; q < 7; q++) {
+      const int c = order[q];
+      if (!plan_step(L[q], __builtin_popcount(c), &c, &c, 1)) return false;
+    }
+    launch_step<T, DEC, 1, LINEAR, LV1, 1>(L[0], s, launches);
+    launch_step<T, DEC, 1, LINEAR, LV1, 2>(L[1], s, launches);
+    launch_step<T, DEC, 1, LINEAR, LV1, 4>(L[2], s, launches);
+    launch_step<T, DEC, 2, LINEAR, LV1, 3>(L[3], s, launches);
+    launch_step<T, DEC, 2, LINEAR, LV1, 5>(L[4], s, launches);
+    launch_step<T, DEC, 2, LINEAR, LV1, 6>(L[5], s, launches);
+    launch_step<T, DEC, 3, LINEAR, LV1, 7>(L[6], s, launches);
     return true;
   }
   // seq1d along seq_order (predictor.py:267-280)
