@@ -246,7 +246,7 @@ __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, 
 // its odd axes (multidim), known at compile time -- every parity test, tap
 // stride and slot term folds; CLSC < 0: classes and axes from the arguments
 template <typename T, bool DEC, int K, bool LINEAR, bool LV1, int CLSC = -1, int TX = txof(K)>
-__global__ void __launch_bounds__(T_THREADS, 2) k_tpass(const __grid_constant__ TPassArgs A,
+__global__ void __launch_bounds__(T_THREADS, CLSC >= 0 ? (K == 3 ? 3 : 4) : 2) k_tpass(const __grid_constant__ TPassArgs A,
                                                          const __grid_constant__ TMaps M) {
   extern __shared__ __align__(128) double tiles[];
   __shared__ unsigned shist[256];
