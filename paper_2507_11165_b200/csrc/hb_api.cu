@@ -32,6 +32,7 @@ struct GraphSlot {
   int nl = 0;
   int nev = 0;                      // profiling marks after the sequence (host bookkeeping
   std::vector<const char*> names;   // of the event-record nodes the graph contains)
+  std::vector<cudaStream_t> streams;
   void reset() {
     if (exec) cudaGraphExecDestroy(exec);
     exec = nullptr;
@@ -59,23 +60,31 @@ struct hb_ctx {
   int nev = 0;
   std::vector<const char*> phase_name;
   std::vector<float> phase_ms;
-  void mark(const char* name) {
+  // second stream: the level passes run on it while the tuner finishes
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_tune[5] = {};
+  std::vector<cudaStream_t> ev_stream;
+  void mark(const char* name) { mark_on(name, stream); }
+  // a phase ends at its mark and starts at the previous mark on the same stream
+  void mark_on(const char* name, cudaStream_t st) {
     if (!prof) return;
     if (nev >= (int)ev.size()) {
       cudaEvent_t e;
       cudaEventCreate(&e);
       ev.push_back(e);
       ev_name.push_back(nullptr);
+      ev_stream.push_back(nullptr);
     }
     // inside a stream capture the record must be external to become an
     // event-record node of the graph (the flag is invalid outside a capture)
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(stream, &cs);
+    cudaStreamIsCapturing(st, &cs);
     if (cs == cudaStreamCaptureStatusActive)
-      cudaEventRecordWithFlags(ev[nev], stream, cudaEventRecordExternal);
+      cudaEventRecordWithFlags(ev[nev], st, cudaEventRecordExternal);
     else
-      cudaEventRecord(ev[nev], stream);
+      cudaEventRecord(ev[nev], st);
     ev_name[nev] = name;
+    ev_stream[nev] = st;
     nev++;
   }
   void collect() {
@@ -83,8 +92,10 @@ struct hb_ctx {
     phase_ms.clear();
     if (!prof) return;
     for (int i = 1; i < nev; i++) {
+      int j = i - 1;
+      while (j > 0 && ev_stream[j] != ev_stream[i]) j--;
       float ms = 0;
-      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      cudaEventElapsedTime(&ms, ev[j], ev[i]);
       phase_name.push_back(ev_name[i]);
       phase_ms.push_back(ms);
     }
@@ -214,7 +225,7 @@ int run_graphed(hb_ctx* ctx, GraphSlot& gs, const std::vector<uint8_t>& key, int
     if (e != cudaSuccess) return set_err(ctx, HB_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(e));
     *nl += gs.nl;
     ctx->nev = gs.nev;
-    for (int i = 0; i < gs.nev; i++) ctx->ev_name[i] = gs.names[i];
+    for (int i = 0; i < gs.nev; i++) ctx->ev_name[i] = gs.names[i], ctx->ev_stream[i] = gs.streams[i];
     return HB_OK;
   }
   if (gs.key == key) {
@@ -246,6 +257,7 @@ int run_graphed(hb_ctx* ctx, GraphSlot& gs, const std::vector<uint8_t>& key, int
   gs.nl = *nl - nl0;
   gs.nev = ctx->nev;
   gs.names.assign(ctx->ev_name.begin(), ctx->ev_name.begin() + ctx->nev);
+  gs.streams.assign(ctx->ev_stream.begin(), ctx->ev_stream.begin() + ctx->nev);
   e = cudaGraphLaunch(gs.exec, s);
   return e == cudaSuccess ? HB_OK : set_err(ctx, HB_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(e));
 }
@@ -549,6 +561,11 @@ void hb_ctx_destroy(hb_ctx* ctx) {
   ctx->g_comp.reset();
   ctx->g_dec.reset();
   if (ctx->enter_ev) cudaEventDestroy(ctx->enter_ev);
+  if (ctx->s2) cudaStreamDestroy(ctx->s2);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  for (auto e : ctx->ev_tune)
+    if (e) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -722,8 +739,110 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
   // 1) error bound (field.py:135-142)
   launch_minmax(dfield, prec, N, st, eb_mode, mag, s, &nl);
   ctx->mark("eb_range");
-  // 2) tuner (tuning.py:105-150)
-  if (tune_global) {
+  // 3)-6): everything after the level walk (and, in the serial form, the
+  // anchors and the levels too) depends only on the buffers, the shape and
+  // the tuned config: one graph-replayable sequence on the main stream
+  auto tail = [&](bool with_levels, const uint8_t* hcfg) -> int {
+    // 3) anchors + the level walk with fused quantize / reorder / histogram
+    const unsigned long long abase = 46 + 8;
+    if (with_levels) launch_anchor_init(dfield, prec, dims, A, E, seq, arch + abase, st, true, s, &nl);
+    static const char* lvl_names[5] = {"", "level1", "level2", "level3", "level4"};
+    for (int level = with_levels ? top : 0; level >= 1; level--) {
+      LevelGeom g;
+      make_level_geom(dims, level, &g);
+      launch_level_compress(g, dfield, prec, E, seq, obm, st, s, &nl, hcfg[level - 1] & 3,
+                            reinterpret_cast<double*>(base + o_scr));
+      ctx->mark(lvl_names[level]);
+    }
+    // 4) outliers straight into the archive (archive.py:65-71)
+    const unsigned long long obase = abase + na * prec + 8;
+    launch_outlier_compact(obm, N, dfield, prec, arch + obase, nullptr, nullptr, lb, st, s, &nl);
+    launch_stream_offset(obase, prec, st, s, &nl);
+    k_set_u64<<<1, 1, 0, s>>>(&st->seq_len, N);
+    nl++;
+    ctx->mark("outliers");
+    unsigned long long* lbx = lb + lb_oc;
+    // 5) lossless pipeline, final record assembled in place at the stream offset
+    if (mode == 0) {
+      launch_huffman_build(st, N, hf, s, &nl);
+      ctx->mark("huff_build");
+      launch_huffman_encode(seq, N, hf, lbx, st, s, &nl);
+      ctx->mark("huff_encode");
+      lbx += lb_he;
+      launch_reduce_chain_impl(2, 4, SRC_MEM, hf, &st->hf_rec_len, 0, cb1.max_words, cb1.rb, &st->bm[0], rre4,
+                               nullptr, &st->scratch[1], lbx, lb_c1, cb1.table, s, &nl);
+      lbx += 4 * lb_c1;
+      launch_reduce_chain_impl(3, 1, SRC_TCMS, rre4, &st->scratch[1], 8, cb2.max_words, cb2.rb, &st->bm[1], arch,
+                               &st->scratch[0], &st->stream_len, lbx, lb_c2, cb2.table, s, &nl);
+    } else {
+      lbx += lb_he;
+      launch_reduce_chain_impl(2, 1, SRC_TP, seq, &st->seq_len, 0, cb1.max_words, cb1.rb, &st->bm[2], arch,
+                               &st->scratch[0], &st->stream_len, lbx, lb_c1, cb1.table, s, &nl);
+    }
+    // 6) escape decision, header, counts (archive.py:55-74)
+    Hdr46 h;
+    memset(&h, 0, sizeof h);
+    memcpy(h.b, "CSZH", 4);
+    h.b[4] = 1;
+    h.b[5] = (uint8_t)mode;
+    h.b[6] = (uint8_t)prec;
+    h.b[7] = (uint8_t)ndim;
+    h.b[8] = (uint8_t)A;
+    for (int a = 0; a < 3; a++)
+      for (int i = 0; i < 8; i++) h.b[14 + 8 * a + i] = (uint8_t)(dims[a] >> (8 * i));
+    uint8_t* d_h = reinterpret_cast<uint8_t*>(&st->scratch[8]);  // 46 bytes inside DevState scratch
+    k_put_hdr46<<<1, 64, 0, s>>>(d_h, h);  // a kernel parameter, not a pinned upload: replay-safe
+    nl++;
+    ctx->mark("lossless");
+    launch_archive_tail_impl(arch, obase, prec, seq, N, d_h, na, st, s, &nl);
+    ctx->mark("archive");
+    return HB_OK;
+  };
+  // 2) tuner (tuning.py:105-150).  Overlapped form: the level passes of
+  // level L run on a second stream as soon as tune level L has picked its
+  // config (a 4-byte read-back per level), while the tuner goes on with
+  // level L-1 on the main stream; the anchors go first on the second stream.
+  const bool overlap = !tune_global && !tune_only && top > 0 && tp.top == top && !getenv("HB_SERIAL_TUNE");
+  if (overlap) {
+    if (!ctx->s2) {
+      CU(cudaStreamCreateWithFlags(&ctx->s2, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+      for (auto& e : ctx->ev_tune) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const cudaStream_t s2 = ctx->s2;
+    CU(cudaEventRecord(ctx->ev_fork, s));
+    CU(cudaStreamWaitEvent(s2, ctx->ev_fork, 0));
+    launch_anchor_init(dfield, prec, dims, A, E, seq, arch + 46 + 8, st, true, s2, &nl);
+    ctx->mark_on("anchors", s2);
+    uint8_t* pc = ctx->pinned + 4096 + 512;
+    for (int level = tp.top; level >= 1; level--) {
+      launch_tune_level(tp, dfield, prec, dims, d_org, level, trials, berr, st, s, &nl);
+      launch_tune_select(tp, level, berr, st, s, &nl);
+      CU(cudaMemcpyAsync(pc + 8 * level, st->cfg, 4, cudaMemcpyDeviceToHost, s));
+      CU(cudaEventRecord(ctx->ev_tune[level], s));
+    }
+    ctx->mark("tune");
+    static const char* lvl_names[5] = {"", "level1", "level2", "level3", "level4"};
+    uint8_t hcfg[4] = {0, 0, 0, 0};
+    for (int level = top; level >= 1; level--) {
+      CU(cudaEventSynchronize(ctx->ev_tune[level]));
+      hcfg[level - 1] = pc[8 * level + level - 1];
+      LevelGeom g;
+      make_level_geom(dims, level, &g);
+      launch_level_compress(g, dfield, prec, E, seq, obm, st, s2, &nl, hcfg[level - 1] & 3,
+                            reinterpret_cast<double*>(base + o_scr));
+      ctx->mark_on(lvl_names[level], s2);
+    }
+    CU(cudaEventRecord(ctx->ev_join, s2));
+    CU(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    ctx->mark("levels");
+    KeyBuf kb;
+    kb.add(dfield).add(prec).add_bytes(dims, 3 * sizeof(uint64_t)).add(ndim).add(mode).add(ctx->arena);
+    kb.add(ctx->arena_size).add(ctx->prof).add(0);
+    rc = run_graphed(ctx, ctx->g_comp, kb.b, &nl, [&]() { return tail(false, hcfg); });
+    if (rc) return rc;
+  } else if (tune_global) {
     auto upfn = [](void* c, void* dev, const void* src, size_t n) -> int {
       PinnedUp* u = reinterpret_cast<PinnedUp*>(c);
       u->off = 8192 + 4096;  // scratch region reused per sub-step (the tuner syncs after each)
@@ -738,79 +857,23 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
       launch_tune_select(tp, level, berr, st, s, &nl);
     }
   }
-  ctx->mark("tune");
+  if (!overlap) ctx->mark("tune");
   // the interpolation config picks the level-kernel instantiation: one small
   // read-back after the tuner (the only mid-call synchronisation)
   uint8_t hcfg[4] = {0, 0, 0, 0};
-  if (!tune_only && top > 0) {
+  if (!overlap && !tune_only && top > 0) {
     uint8_t* pc = ctx->pinned + 4096 + 512;
     CU(cudaMemcpyAsync(pc, st->cfg, 4, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     memcpy(hcfg, pc, 4);
   }
-  if (!tune_only) {
+  if (!overlap && !tune_only) {
     // 3)-6): everything after the tuner depends only on the buffers, the
     // shape and the tuned config, so it is one (graph-replayable) sequence
-    auto tail = [&]() -> int {
-      // 3) anchors + the level walk with fused quantize / reorder / histogram
-      const unsigned long long abase = 46 + 8;
-      launch_anchor_init(dfield, prec, dims, A, E, seq, arch + abase, st, true, s, &nl);
-      static const char* lvl_names[5] = {"", "level1", "level2", "level3", "level4"};
-      for (int level = top; level >= 1; level--) {
-        LevelGeom g;
-        make_level_geom(dims, level, &g);
-        launch_level_compress(g, dfield, prec, E, seq, obm, st, s, &nl, hcfg[level - 1] & 3,
-                              reinterpret_cast<double*>(base + o_scr));
-        ctx->mark(lvl_names[level]);
-      }
-      // 4) outliers straight into the archive (archive.py:65-71)
-      const unsigned long long obase = abase + na * prec + 8;
-      launch_outlier_compact(obm, N, dfield, prec, arch + obase, nullptr, nullptr, lb, st, s, &nl);
-      launch_stream_offset(obase, prec, st, s, &nl);
-      k_set_u64<<<1, 1, 0, s>>>(&st->seq_len, N);
-      nl++;
-      ctx->mark("outliers");
-      unsigned long long* lbx = lb + lb_oc;
-      // 5) lossless pipeline, final record assembled in place at the stream offset
-      if (mode == 0) {
-        launch_huffman_build(st, N, hf, s, &nl);
-        ctx->mark("huff_build");
-        launch_huffman_encode(seq, N, hf, lbx, st, s, &nl);
-        ctx->mark("huff_encode");
-        lbx += lb_he;
-        launch_reduce_chain_impl(2, 4, SRC_MEM, hf, &st->hf_rec_len, 0, cb1.max_words, cb1.rb, &st->bm[0], rre4,
-                                 nullptr, &st->scratch[1], lbx, lb_c1, cb1.table, s, &nl);
-        lbx += 4 * lb_c1;
-        launch_reduce_chain_impl(3, 1, SRC_TCMS, rre4, &st->scratch[1], 8, cb2.max_words, cb2.rb, &st->bm[1], arch,
-                                 &st->scratch[0], &st->stream_len, lbx, lb_c2, cb2.table, s, &nl);
-      } else {
-        lbx += lb_he;
-        launch_reduce_chain_impl(2, 1, SRC_TP, seq, &st->seq_len, 0, cb1.max_words, cb1.rb, &st->bm[2], arch,
-                                 &st->scratch[0], &st->stream_len, lbx, lb_c1, cb1.table, s, &nl);
-      }
-      // 6) escape decision, header, counts (archive.py:55-74)
-      Hdr46 h;
-      memset(&h, 0, sizeof h);
-      memcpy(h.b, "CSZH", 4);
-      h.b[4] = 1;
-      h.b[5] = (uint8_t)mode;
-      h.b[6] = (uint8_t)prec;
-      h.b[7] = (uint8_t)ndim;
-      h.b[8] = (uint8_t)A;
-      for (int a = 0; a < 3; a++)
-        for (int i = 0; i < 8; i++) h.b[14 + 8 * a + i] = (uint8_t)(dims[a] >> (8 * i));
-      uint8_t* d_h = reinterpret_cast<uint8_t*>(&st->scratch[8]);  // 46 bytes inside DevState scratch
-      k_put_hdr46<<<1, 64, 0, s>>>(d_h, h);  // a kernel parameter, not a pinned upload: replay-safe
-      nl++;
-      ctx->mark("lossless");
-      launch_archive_tail_impl(arch, obase, prec, seq, N, d_h, na, st, s, &nl);
-      ctx->mark("archive");
-      return HB_OK;
-    };
     KeyBuf kb;
     kb.add(dfield).add(prec).add_bytes(dims, 3 * sizeof(uint64_t)).add(ndim).add(mode).add(ctx->arena);
-    kb.add(ctx->arena_size).add_bytes(hcfg, 4).add(ctx->prof);
-    rc = run_graphed(ctx, ctx->g_comp, kb.b, &nl, tail);
+    kb.add(ctx->arena_size).add_bytes(hcfg, 4).add(ctx->prof).add(1);
+    rc = run_graphed(ctx, ctx->g_comp, kb.b, &nl, [&]() { return tail(true, hcfg); });
     if (rc) return rc;
   }
   ctx->launches = nl;
