@@ -1409,16 +1409,19 @@ struct BitReader {
   }
 };
 
-// 16-byte aligned output writer for one thread's contiguous output range
+// 16-byte aligned output writer for one thread's contiguous output range.
+// The current window is pre-filled with the run symbol, so a run of that
+// symbol only advances the position; other bytes replace their slots.
 struct OutWriter {
   uint8_t* out;
   unsigned long long start, p;
-  uint64_t lo, hi;
+  uint64_t lo, hi, rep;
   unsigned zeros;
-  __device__ void init(uint8_t* o, unsigned long long s) {
+  __device__ void init(uint8_t* o, unsigned long long s, int fill) {
     out = o;
     start = p = s;
-    lo = hi = 0;
+    rep = 0x0101010101010101ull * (uint64_t)(fill & 0xFF);
+    lo = hi = rep;
     zeros = 0;
   }
   __device__ __forceinline__ void flush_chunk(unsigned long long base, int upto) {  // bytes [base, base+upto)
@@ -1431,64 +1434,148 @@ struct OutWriter {
         out[base + k] = (uint8_t)(k < 8 ? (lo >> (8 * k)) : (hi >> (8 * (k - 8))));
       }
     }
-    lo = hi = 0;
+    lo = hi = rep;
+  }
+  // advance over z bytes equal to the fill byte: complete windows go out as
+  // they are crossed (the ones wholly inside the run are pure fill)
+  __device__ __forceinline__ void skip_fill(unsigned long long z) {
+    const unsigned long long q = p + z;
+    unsigned long long wb = p & ~15ull;
+    while (wb + 16 <= q) {
+      flush_chunk(wb, 16);
+      wb += 16;
+    }
+    p = q;
   }
   __device__ __forceinline__ void put(int b) {
     const int k = (int)(p & 15);
+    const uint64_t m = 0xFFull << (8 * (k & 7));
+    const uint64_t v = (uint64_t)(b & 0xFF) << (8 * (k & 7));
     if (k < 8)
-      lo |= (uint64_t)b << (8 * k);
+      lo = (lo & ~m) | v;
     else
-      hi |= (uint64_t)b << (8 * (k - 8));
+      hi = (hi & ~m) | v;
     p++;
     if (!(p & 15)) flush_chunk(p - 16, 16);
   }
-  // n (<= 4) packed bytes, first in the low byte, in one or two shifts
+  // n (<= 4) packed bytes, first in the low byte, replacing window bytes
   __device__ __forceinline__ void put4(uint32_t pk, int n) {
-    const uint64_t v = n >= 4 ? (uint64_t)pk : ((uint64_t)pk & ((1ull << (8 * n)) - 1));
+    const uint64_t nm = n >= 4 ? 0xFFFFFFFFull : ((1ull << (8 * n)) - 1);
+    const uint64_t v = (uint64_t)pk & nm;
     const int k = (int)(p & 15);
     const int e = k + n;  // window bytes [k, e)
     if (k < 8) {
-      lo |= v << (8 * k);
-      if (e > 8) hi |= v >> (64 - 8 * k);  // k > 4 here, shift < 64
+      lo = (lo & ~(nm << (8 * k))) | (v << (8 * k));
+      if (e > 8) hi = (hi & ~(nm >> (64 - 8 * k))) | (v >> (64 - 8 * k));  // k > 4 here, shift < 64
     } else {
-      hi |= v << (8 * (k - 8));
+      hi = (hi & ~(nm << (8 * (k - 8)))) | (v << (8 * (k - 8)));
     }
     p += n;
     if (e >= 16) {
       // window complete: flush, then carry the bytes that spilled past byte 15
       flush_chunk(p - e, 16);
-      if (e > 16) lo = v >> (8 * (16 - k));
+      if (e > 16) {
+        const int sp = 8 * (16 - k);
+        lo = (rep & ~(nm >> sp)) | (v >> sp);
+      }
     }
   }
-  // n copies of byte b: masked fill of the current 16-byte window, whole
-  // windows as single 16-byte stores
+  // n copies of byte b
   __device__ __forceinline__ void run(int b, unsigned long long n) {
-    const uint64_t rep = 0x0101010101010101ull * (uint64_t)b;
+    const uint64_t r = 0x0101010101010101ull * (uint64_t)b;
     while (n) {
       const int k = (int)(p & 15);
       const int take = n < (unsigned long long)(16 - k) ? (int)n : 16 - k;
-      if (k == 0 && take == 16) {
-        lo = hi = rep;
-        flush_chunk(p, 16);
-      } else {
-        // bytes [k, k+take) of the window
-        const int a = k, e = k + take;
-        const uint64_t mlo = (a < 8) ? ((e >= 8 ? ~0ull : ((1ull << (8 * e)) - 1)) & (~0ull << (8 * a))) : 0ull;
-        const uint64_t mhi = (e > 8) ? ((e >= 16 ? ~0ull : ((1ull << (8 * (e - 8))) - 1)) &
-                                        (a <= 8 ? ~0ull : (~0ull << (8 * (a - 8)))))
-                                     : 0ull;
-        lo |= rep & mlo;
-        hi |= rep & mhi;
-        if (e == 16) flush_chunk(p - k, 16);
-      }
+      const int a = k, e = k + take;  // bytes [a, e) of the window
+      const uint64_t mlo = (a < 8) ? ((e >= 8 ? ~0ull : ((1ull << (8 * e)) - 1)) & (~0ull << (8 * a))) : 0ull;
+      const uint64_t mhi = (e > 8) ? ((e >= 16 ? ~0ull : ((1ull << (8 * (e - 8))) - 1)) &
+                                      (a <= 8 ? ~0ull : (~0ull << (8 * (a - 8)))))
+                                   : 0ull;
+      lo = (lo & ~mlo) | (r & mlo);
+      hi = (hi & ~mhi) | (r & mhi);
       p += take;
       n -= take;
+      if (e == 16) flush_chunk(p - 16, 16);
     }
   }
   __device__ void finish() {
     if (p & 15) flush_chunk(p & ~15ull, (int)(p & 15));
   }
 };
+
+// Fast loop for streams whose most frequent symbol has the 1-bit code "0"
+// (stages.py:293-302 canonical codes: that code is all zeros): consume the
+// leading-zero run with one clz, then decode at the '1' bit through the
+// multi-symbol table (slow path for long codes / the stop bound).  Returns
+// nonzero on a decode error (pos at the failing codeword).
+template <bool EMIT>
+__device__ __forceinline__ int hd_fast(const HDTables& T, const HDShared* S, BitReader& br, unsigned long long& pos,
+                                       const unsigned long long lim, long long& cnt, OutWriter* ow) {
+  const int K = T.K, rs = T.run_sym;
+  while (pos < lim) {
+    unsigned long long z = br.buf ? (unsigned long long)__clzll(br.buf) : 64ull;
+    bool capped = false;
+    if (z >= (unsigned long long)br.nb) {
+      z = br.nb;
+      capped = true;
+    }
+    if (z >= lim - pos) {
+      z = lim - pos;
+      capped = true;
+    }
+    if (z) {
+      if (EMIT) {
+        ow->skip_fill(z);
+        if (rs == 0) ow->zeros += (unsigned)z;
+      }
+      pos += z;
+      cnt += (long long)z;
+      br.consume((int)z);
+    }
+    if (capped) continue;  // at the stop bound, or the run goes on past the buffer
+    const unsigned key = (unsigned)(br.buf >> (64 - K));
+    const uint8_t mm = S->mmeta[key];
+    const int n = mm & 7, b = mm >> 3;
+    if (n >= 1 && pos + b <= lim) {
+      if (EMIT) {
+        const uint32_t pk = S->msym[key];
+        ow->put4(pk, n);
+        const uint32_t live = n >= 4 ? 0xFFFFFFFFu : ((1u << (8 * n)) - 1);
+        ow->zeros += (unsigned)__popc(__vcmpeq4(pk, 0u) & live) >> 3;
+      }
+      pos += b;
+      cnt += n;
+      br.consume(b);
+      continue;
+    }
+    const uint16_t e = S->lut[key];
+    int L, sym;
+    if (e) {
+      L = e >> 8;
+      sym = e & 0xFF;
+    } else {
+      sym = -1;
+      for (L = K + 1; L <= T.maxlen; L++) {
+        if (!T.count[L]) continue;
+        const unsigned long long c = br.peek(L);
+        if (c >= T.first_code[L] && c - T.first_code[L] < (unsigned long long)T.count[L]) {
+          sym = T.syms[T.first_rank[L] + (int)(c - T.first_code[L])];
+          break;
+        }
+      }
+      if (sym < 0) return 1;
+    }
+    if (pos + L > T.nbits) return 1;
+    if (EMIT) {
+      ow->put(sym);
+      ow->zeros += sym == 0;
+    }
+    pos += L;
+    cnt++;
+    br.consume(L);
+  }
+  return 0;
+}
 
 // decode from `start` while pos < stop (and < nbits); returns symbols or -1 on error.
 // MASK: record codeword starts in [start, start+64) into *mask.
@@ -1507,6 +1594,17 @@ __device__ long long hd_decode(const HDTables& T, const HDShared* S, const uint8
   const unsigned long long lim = stop < T.nbits ? stop : T.nbits;
   const int K = T.K, rs = T.run_sym;
   while (pos < lim) {
+    if (EMIT && !SYNC && rs >= 0) {
+      // emitting a smooth stream: every step = one run of the 1-bit code "0"
+      // (possibly empty; a pure position advance for the writer) + one table
+      // step at the next '1' bit, the same instruction sequence for every lane
+      if (hd_fast<EMIT>(T, S, br, pos, lim, cnt, ow)) {
+        *endp = pos;
+        if (MASK) *mask = m;
+        return -1;
+      }
+      break;
+    }
     if (SYNC) {
       const unsigned long long q = pos - sbase;
       if (q >= 64) break;  // no sync inside the window
@@ -1739,7 +1837,7 @@ __global__ void __launch_bounds__(256) k_hd_emit(const uint8_t* rec, const HDTab
       continue;
     }
     OutWriter ow;
-    ow.init(out, W.off[i]);
+    ow.init(out, W.off[i], T->run_sym >= 0 ? T->run_sym : 0);
     unsigned long long e;
     const long long c = hd_decode<true>(*T, &S, pay, s0, (i + 1) * HD_S, &e, &ow);
     ow.finish();
