@@ -1817,7 +1817,7 @@ __global__ void __launch_bounds__(256) k_hd_scan(const HDTables* T, HDWork W, in
   }
 }
 
-__global__ void __launch_bounds__(256) k_hd_emit(const uint8_t* rec, const HDTables* T, HDWork W, int fin,
+__global__ void __launch_bounds__(256, 4) k_hd_emit(const uint8_t* rec, const HDTables* T, HDWork W, int fin,
                                                  uint8_t* out, DevState* st) {
   __shared__ HDShared S;
   if (!T->ok) return;
