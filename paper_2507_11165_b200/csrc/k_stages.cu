@@ -77,7 +77,8 @@ struct MemSrc {  // plain bytes
     return v;
   }
   // words [i0, i0+32) (i0 % 32 == 0), zero past the end
-  __device__ void load32(unsigned long long i0, uint64_t* v) const {
+  template <typename T>
+  __device__ void load32(unsigned long long i0, T* v) const {
     const unsigned long long o = i0 * w;
     if (o + 32ull * w <= len && !((uintptr_t)(p + o) & 15)) {
       const uint4* q = reinterpret_cast<const uint4*>(p + o);
@@ -98,7 +99,7 @@ struct MemSrc {  // plain bytes
       }
     }
 #pragma unroll
-    for (int j = 0; j < 32; j++) v[j] = word(i0 + j);
+    for (int j = 0; j < 32; j++) v[j] = (T)word(i0 + j);
   }
 };
 
@@ -124,7 +125,8 @@ struct TcmsSrc {
     return (zz(u, tw) >> (8 * r)) & 0xFF;
   }
   __device__ unsigned long long len() const { return 10 + cdiv(n, tw) * tw; }
-  __device__ void load32(unsigned long long i0, uint64_t* v) const {
+  template <typename T>
+  __device__ void load32(unsigned long long i0, T* v) const {
     if (tw == 8 && i0 >= 32) {  // bytes [i0, i0+32) = words (i0-10)/8 .. +4 of zz(data)
       const unsigned long long q0 = (i0 - 10) >> 3;  // (i0-10) % 8 == 6
       uint64_t z[5];
@@ -142,12 +144,12 @@ struct TcmsSrc {
 #pragma unroll
       for (int j = 0; j < 32; j++) {
         const int b = 6 + j;  // byte position from word q0
-        v[j] = (z[b >> 3] >> (8 * (b & 7))) & 0xFF;
+        v[j] = (T)((z[b >> 3] >> (8 * (b & 7))) & 0xFF);
       }
       return;
     }
 #pragma unroll
-    for (int j = 0; j < 32; j++) v[j] = word(i0 + j);
+    for (int j = 0; j < 32; j++) v[j] = (T)word(i0 + j);
   }
 };
 
@@ -194,7 +196,8 @@ struct TpSrc {
     return bit_plane(tcms_group(t), (int)((j - 10) & 7));
   }
   __device__ unsigned long long len() const { return 10 + cdiv(n + 10, 8) * 8; }
-  __device__ void load32(unsigned long long i0, uint64_t* v) const {
+  template <typename T>
+  __device__ void load32(unsigned long long i0, T* v) const {
     if (i0 >= 32) {  // record bytes [i0, i0+32) = planes of tiles (i0-10)/8 .. +4
       const unsigned long long t0 = (i0 - 10) >> 3;  // (i0-10) % 8 == 6
       uint64_t g[5];
@@ -203,21 +206,24 @@ struct TpSrc {
 #pragma unroll
       for (int j = 0; j < 32; j++) {
         const int b = 6 + j;
-        v[j] = bit_plane(g[b >> 3], b & 7);
+        v[j] = (T)bit_plane(g[b >> 3], b & 7);
       }
       return;
     }
 #pragma unroll
-    for (int j = 0; j < 32; j++) v[j] = word(i0 + j);
+    for (int j = 0; j < 32; j++) v[j] = (T)word(i0 + j);
   }
 };
 
 // ------------------------------------------------------- reducer encode
 // stages.py:165-184.  stage 2 = RRE (keep w[i] != w[i-1]), 3 = RZE (w != 0).
 
-template <class Src>
+// WT: register word type (32-bit for widths <= 4: half the registers).
+// stg: shared staging for the tile's kept words (widths <= 4), written out
+// with coalesced stores once the tile's base is known; null = direct stores.
+template <class Src, typename WT>
 __device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage, int width, uint8_t* bitmap,
-                             uint8_t* payload, unsigned long long* lb, BmLevel* lv) {
+                             uint8_t* payload, unsigned long long* lb, BmLevel* lv, uint8_t* stg) {
   __shared__ unsigned long long sh[33];
   __shared__ unsigned long long tile_sh, base_sh;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -231,12 +237,12 @@ __device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage, i
     if (tile >= ntiles) break;
     // each lane owns 32 consecutive words: independent loads, one bitmap word
     const unsigned long long i0 = tile * RD_TILE + (unsigned long long)wid * 1024 + (unsigned long long)lane * 32;
-    uint64_t v[32];
+    WT v[32];
     uint32_t mask = 0;
     if (i0 < nw) {
       src.load32(i0, v);
-      uint64_t prev = 0;
-      if (stage == 2) prev = i0 > 0 ? src.word(i0 - 1) : ~v[0];
+      WT prev = 0;
+      if (stage == 2) prev = i0 > 0 ? (WT)src.word(i0 - 1) : (WT)~v[0];
 #pragma unroll
       for (int j = 0; j < 32; j++) {
         const bool in = i0 + j < nw;
@@ -254,22 +260,54 @@ __device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage, i
       const unsigned long long ex_ = lookback_warp(status, tile, total);
       if (threadIdx.x == 0) base_sh = ex_;
     }
-    __syncthreads();
-    unsigned long long dst = base_sh + wex + incl - c;
-    if (mask) {
+    if (stg) {
+      // kept words into shared memory at their tile-local rank
+      unsigned d = (unsigned)(wex + incl - c);
+      if (mask) {
 #pragma unroll
-      for (int j = 0; j < 32; j++) {
-        if ((mask >> (31 - j)) & 1) {
-          uint8_t* p = payload + dst * width;
-          if (width == 1)
-            *p = (uint8_t)v[j];
-          else if (width == 2)
-            *reinterpret_cast<uint16_t*>(p) = (uint16_t)v[j];
-          else if (width == 4)
-            *reinterpret_cast<uint32_t*>(p) = (uint32_t)v[j];
-          else
-            *reinterpret_cast<uint64_t*>(p) = v[j];
-          dst++;
+        for (int j = 0; j < 32; j++) {
+          if ((mask >> (31 - j)) & 1) {
+            if (width == 1)
+              stg[d] = (uint8_t)v[j];
+            else if (width == 2)
+              reinterpret_cast<uint16_t*>(stg)[d] = (uint16_t)v[j];
+            else
+              reinterpret_cast<uint32_t*>(stg)[d] = (uint32_t)v[j];
+            d++;
+          }
+        }
+      }
+      __syncthreads();
+      const unsigned long long base = base_sh;
+      const unsigned tot = (unsigned)total;
+      if (width == 4) {
+        uint32_t* o = reinterpret_cast<uint32_t*>(payload) + base;
+        for (unsigned i = threadIdx.x; i < tot; i += blockDim.x) o[i] = reinterpret_cast<const uint32_t*>(stg)[i];
+      } else if (width == 2) {
+        uint16_t* o = reinterpret_cast<uint16_t*>(payload) + base;
+        for (unsigned i = threadIdx.x; i < tot; i += blockDim.x) o[i] = reinterpret_cast<const uint16_t*>(stg)[i];
+      } else {
+        uint8_t* o = payload + base;
+        for (unsigned i = threadIdx.x; i < tot; i += blockDim.x) o[i] = stg[i];
+      }
+    } else {
+      __syncthreads();
+      unsigned long long dst = base_sh + wex + incl - c;
+      if (mask) {
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+          if ((mask >> (31 - j)) & 1) {
+            uint8_t* p = payload + dst * width;
+            if (width == 1)
+              *p = (uint8_t)v[j];
+            else if (width == 2)
+              *reinterpret_cast<uint16_t*>(p) = (uint16_t)v[j];
+            else if (width == 4)
+              *reinterpret_cast<uint32_t*>(p) = (uint32_t)v[j];
+            else
+              *reinterpret_cast<uint64_t*>(p) = (uint64_t)v[j];
+            dst++;
+          }
         }
       }
     }
@@ -279,10 +317,11 @@ __device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage, i
 }
 
 // level 0 of a chain over a typed source
-template <class Src>
-__global__ void __launch_bounds__(RD_THREADS)
+template <class Src, typename WT>
+__global__ void __launch_bounds__(RD_THREADS, sizeof(WT) == 4 ? 4 : 1)
     k_reduce0(Src src, const unsigned long long* len_dev, int stage, int width, BmState* bm, uint8_t* bitmap,
               uint8_t* payload, unsigned long long* lb) {
+  extern __shared__ __align__(16) uint8_t rd_stg[];
   Src s2 = src;
   unsigned long long len;
   if constexpr (sizeof(Src) == sizeof(MemSrc) && __is_same(Src, MemSrc)) {
@@ -303,13 +342,14 @@ __global__ void __launch_bounds__(RD_THREADS)
     lv->bm_len = cdiv(nw, 8);
     lv->active = 1;
   }
-  reduce_tiles(s2, nw, stage, width, bitmap, payload, lb, lv);
+  reduce_tiles<Src, WT>(s2, nw, stage, width, bitmap, payload, lb, lv, width <= 4 ? rd_stg : nullptr);
 }
 
 // nested RRE1 over the previous level's bitmap (stages.py:178-181)
-__global__ void __launch_bounds__(RD_THREADS)
+__global__ void __launch_bounds__(RD_THREADS, 4)
     k_reduce_nested(int level, BmState* bm, const uint8_t* prev_bitmap, uint8_t* bitmap, uint8_t* payload,
                     unsigned long long* lb) {
+  __shared__ __align__(16) uint8_t stg[RD_TILE];
   const BmLevel* p = &bm->lv[level - 1];
   if (!p->active || p->bm_len <= 19) return;
   MemSrc src{prev_bitmap, p->bm_len, 1};
@@ -321,7 +361,7 @@ __global__ void __launch_bounds__(RD_THREADS)
     lv->bm_len = cdiv(nw, 8);
     lv->active = 1;
   }
-  reduce_tiles(src, nw, 2, 1, bitmap, payload, lb, lv);
+  reduce_tiles<MemSrc, uint32_t>(src, nw, 2, 1, bitmap, payload, lb, lv, stg);
 }
 
 // dst[0..n) = src[0..n) for a 4-byte aligned src and any dst: aligned 32-bit
@@ -432,18 +472,30 @@ void launch_reduce_chain_impl(int stage, int width, int src_kind, const uint8_t*
                               cudaStream_t s, int* launches) {
   const unsigned long long tiles0 = cdiv(max_words, RD_TILE);
   const unsigned g0 = persist_grid(tiles0);
+  const size_t stg = width <= 4 ? (size_t)RD_TILE * width : 0;
   switch (src_kind) {
     case SRC_MEM:
-      k_reduce0<MemSrc><<<g0, RD_THREADS, 0, s>>>(MemSrc{src_ptr, 0, width}, len_dev, stage, width, bm,
-                                                  bufs.bitmap[0], bufs.payload[0], lb_ws);
+      if (width <= 4) {
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(k_reduce0<MemSrc, uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               RD_TILE * 4);
+          attr = true;
+        }
+        k_reduce0<MemSrc, uint32_t><<<g0, RD_THREADS, stg, s>>>(MemSrc{src_ptr, 0, width}, len_dev, stage, width,
+                                                                bm, bufs.bitmap[0], bufs.payload[0], lb_ws);
+      } else {
+        k_reduce0<MemSrc, uint64_t><<<g0, RD_THREADS, 0, s>>>(MemSrc{src_ptr, 0, width}, len_dev, stage, width, bm,
+                                                              bufs.bitmap[0], bufs.payload[0], lb_ws);
+      }
       break;
     case SRC_TCMS:
-      k_reduce0<TcmsSrc><<<g0, RD_THREADS, 0, s>>>(TcmsSrc{src_ptr, 0, tw}, len_dev, stage, width, bm,
-                                                   bufs.bitmap[0], bufs.payload[0], lb_ws);
+      k_reduce0<TcmsSrc, uint32_t><<<g0, RD_THREADS, stg, s>>>(TcmsSrc{src_ptr, 0, tw}, len_dev, stage, width, bm,
+                                                               bufs.bitmap[0], bufs.payload[0], lb_ws);
       break;
     default:
-      k_reduce0<TpSrc><<<g0, RD_THREADS, 0, s>>>(TpSrc{src_ptr, 0}, len_dev, stage, width, bm, bufs.bitmap[0],
-                                                 bufs.payload[0], lb_ws);
+      k_reduce0<TpSrc, uint32_t><<<g0, RD_THREADS, stg, s>>>(TpSrc{src_ptr, 0}, len_dev, stage, width, bm,
+                                                             bufs.bitmap[0], bufs.payload[0], lb_ws);
       break;
   }
   (*launches)++;
