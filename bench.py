@@ -235,7 +235,10 @@ def run_ours(args):
     assert err <= info["abs_eb"], (err, info["abs_eb"])
     archive_len = arch.numel()
 
-    _lib.set_profile(True)
+    # timed region: only the level-pass marks (the dominant kernel's CUDA
+    # events for the roofline); the full phase table comes from an untimed
+    # profiled pass afterwards
+    _lib.set_profile(2)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     phases = {}
     launches = 0
@@ -272,6 +275,17 @@ def run_ours(args):
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    timed_phases = phases
+    phases = {}
+    _lib.set_profile(True)
+    for _ in range(2):
+        a = hb.compress_device(f, spec, args.mode, out=out_buf)
+        for nm, ms in _lib.last_phases():
+            phases.setdefault(nm, []).append(ms)
+        hb.decompress_device(a, f.dims, np.float32, out=rec_buf)
+        for nm, ms in _lib.last_phases():
+            phases.setdefault(nm, []).append(ms)
+    torch.cuda.synchronize()
     _lib.set_profile(False)
     tc = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3
     td = sum(e[1].elapsed_time(e[2]) for e in ev) / 1e3
@@ -284,7 +298,7 @@ def run_ours(args):
 
     # roofline of the dominant kernel (CUDA events around it on the launch stream)
     peak, peak_kind = peaks()
-    cand = {k: statistics.mean(v) for k, v in phases.items() if algo_bytes(k, n, 4, archive_len) > 0}
+    cand = {k: statistics.mean(v) for k, v in timed_phases.items() if algo_bytes(k, n, 4, archive_len) > 0}
     dom = max(cand, key=cand.get) if cand else None
     roof = None
     if dom:

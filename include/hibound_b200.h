@@ -72,8 +72,9 @@ HB_API const char* hb_last_error(const hb_ctx* ctx);
 /* kernels launched by the last call (for the bench's gpu_launches claim) */
 HB_API uint64_t hb_last_launch_count(const hb_ctx* ctx);
 
-/* Optional per-phase device timing (CUDA events on the context stream) of
- * the last compress / decompress; names are static strings. */
+/* Optional per-phase device timing (CUDA events on the context streams) of
+ * the last compress / decompress; names are static strings.  enable: 0 off,
+ * 1 every phase, 2 only the level passes (level1..4 / rlevel1..4). */
 HB_API void hb_profile(hb_ctx* ctx, int enable);
 HB_API int hb_last_phases(const hb_ctx* ctx, const char** names, float* ms, int cap);
 

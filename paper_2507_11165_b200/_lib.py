@@ -149,8 +149,10 @@ def is_cuda(x) -> bool:
     return t is not None and isinstance(x, t.Tensor) and x.is_cuda
 
 
-def set_profile(enable: bool):
-    lib().hb_profile(ctx(), 1 if enable else 0)
+def set_profile(enable):
+    """True/1: CUDA-event marks at every phase; 2: only the level-pass marks
+    (the cheap form used inside bench.py's timed region); False/0: off."""
+    lib().hb_profile(ctx(), 2 if enable == 2 else (1 if enable else 0))
 
 
 def last_phases() -> list:
