@@ -523,6 +523,41 @@ struct Hdr46 {
   uint8_t b[46];
 };
 
+// device-resident archive: bytes [0, 64) plus the outlier count and the
+// stream length found by the same section walk as parse_info_t (offsets
+// ~0 where the walk leaves the archive; the host walk reports the error)
+__global__ void k_peek_walk(const uint8_t* a, unsigned long long len, uint8_t* out) {
+  const unsigned long long m = len < 64 ? len : 64;
+  for (unsigned long long i = threadIdx.x; i < m; i += blockDim.x) out[i] = a[i];
+  if (threadIdx.x) return;
+  auto u64 = [&](unsigned long long o) {
+    unsigned long long v = 0;
+    for (int i = 0; i < 8; i++) v |= (unsigned long long)a[o + i] << (8 * i);
+    return v;
+  };
+  unsigned long long r[4] = {~0ull, 0, ~0ull, 0};
+  if (len >= 54) {
+    const unsigned prec = a[6];
+    const unsigned long long na = u64(46);
+    if ((prec == 4 || prec == 8) && na <= len) {
+      const unsigned long long oc_off = 54 + na * prec;
+      if (oc_off <= len && len - oc_off >= 8) {
+        r[0] = oc_off;
+        r[1] = u64(oc_off);
+        if (r[1] <= len) {
+          const unsigned long long sl_off = oc_off + 8 + r[1] * (8 + prec);
+          if (sl_off <= len && len - sl_off >= 8) {
+            r[2] = sl_off;
+            r[3] = u64(sl_off);
+          }
+        }
+      }
+    }
+  }
+  for (int k = 0; k < 4; k++)
+    for (int i = 0; i < 8; i++) out[64 + 8 * k + i] = (uint8_t)(r[k] >> (8 * i));
+}
+
 __global__ void k_put_hdr46(uint8_t* dst, Hdr46 h) {
   if (threadIdx.x < 46) dst[threadIdx.x] = h.b[threadIdx.x];
 }
@@ -986,26 +1021,34 @@ int hb_decompress(hb_ctx* ctx, const void* archive, size_t len, void* field_out,
   if (host_arch) {
     rc = parse_info((const uint8_t*)archive, len, &I, ctx);
   } else {
-    // header fields live in device memory: fetch the few bytes the walk needs
-    // through the pinned buffer (async copy + stream sync); the first read
-    // brings the header and the anchor count (bytes [0, 54)) in one trip
+    // header fields live in device memory: one kernel walks the section
+    // offsets on the device and drops the bytes the host walk needs (header,
+    // anchor / outlier counts, stream length) into pinned memory, one sync
     if ((rc = ensure_pinned(ctx, 1 << 16))) return rc;
     uint8_t* pin = ctx->pinned + 4096 + 1024;
-    size_t have = 0;
+    k_peek_walk<<<1, 64, 0, s>>>((const uint8_t*)archive, len, pin);
+    {
+      const cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return set_err(ctx, HB_ECUDA, "header read: %s", cudaGetErrorString(e));
+    }
+    uint64_t pk[4];
+    memcpy(pk, pin + 64, 32);  // outlier-count offset, count, stream-length offset, length
+    const size_t have = std::min<size_t>(len, 64);
     rc = parse_info_t(
         [&](size_t off, size_t n, uint8_t* dst) -> int {
           if (off + n <= have) {
             memcpy(dst, pin + off, n);
             return 0;
           }
-          const bool head = off == 0;
-          const size_t m = head ? std::min<size_t>(len, 64) : n;
-          cudaError_t e = cudaMemcpyAsync(head ? pin : pin + 512, (const uint8_t*)archive + off, m,
-                                          cudaMemcpyDeviceToHost, ctx->stream);
-          if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+          if (n == 8 && (off == pk[0] || off == pk[2])) {
+            memcpy(dst, off == pk[0] ? &pk[1] : &pk[3], 8);
+            return 0;
+          }
+          uint8_t* tmp = pin + 512;
+          cudaError_t e = cudaMemcpyAsync(tmp, (const uint8_t*)archive + off, n, cudaMemcpyDeviceToHost, s);
+          if (e == cudaSuccess) e = cudaStreamSynchronize(s);
           if (e != cudaSuccess) return set_err(ctx, HB_ECUDA, "header read: %s", cudaGetErrorString(e));
-          if (head) have = m;
-          memcpy(dst, head ? pin : pin + 512, n);
+          memcpy(dst, tmp, n);
           return 0;
         },
         len, &I, ctx);
