@@ -890,8 +890,7 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
     uint8_t* pc = ctx->pinned + 4096 + 512;
     for (int level = tp.top; level >= 1; level--) {
       launch_tune_level(tp, dfield, prec, dims, d_org, level, trials, berr, st, s, &nl);
-      launch_tune_select(tp, level, berr, st, s, &nl);
-      CU(cudaMemcpyAsync(pc + 8 * level, st->cfg, 4, cudaMemcpyDeviceToHost, s));
+      launch_tune_select(tp, level, berr, st, s, &nl, pc);
       CU(cudaEventRecord(ctx->ev_tune[level], s));
     }
     ctx->mark("tune");
@@ -899,7 +898,7 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
     uint8_t hcfg[4] = {0, 0, 0, 0};
     for (int level = top; level >= 1; level--) {
       CU(cudaEventSynchronize(ctx->ev_tune[level]));
-      hcfg[level - 1] = pc[8 * level + level - 1];
+      hcfg[level - 1] = reinterpret_cast<volatile uint8_t*>(pc)[level - 1];
       LevelGeom g;
       make_level_geom(dims, level, &g);
       launch_level_compress(g, dfield, prec, E, seq, obm, st, s2, &nl, hcfg[level - 1] & 3,

@@ -92,7 +92,8 @@ void launch_tune_level(const TunePlan& p, const void* field, int prec, const uin
                        const unsigned long long* origins, int level, double* trials, double* berr, DevState* st,
                        cudaStream_t s, int* launches);
 void launch_tune_select(const TunePlan& p, int level, const double* berr, DevState* st, cudaStream_t s,
-                        int* launches);
+                        int* launches,
+                        uint8_t* host_cfg = nullptr);
 // whole-field blocks too large for shared memory
 size_t tune_global_bytes(unsigned long long bn);
 int launch_tune_global(const void* field, int prec, const uint64_t dims[3], int top, uint8_t* scratch,

@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(TUNE_THREADS)
 }
 
 // tuning.py:135-140
-__global__ void k_tune_select(int nb, int level, const double* berr, DevState* st) {
+__global__ void k_tune_select(int nb, int level, const double* berr, DevState* st, uint8_t* host_cfg) {
   __shared__ double e[4];
   const int ci = threadIdx.x;
   if (ci < 4) {
@@ -269,6 +269,10 @@ __global__ void k_tune_select(int nb, int level, const double* berr, DevState* s
       if (e[i] < e[best]) best = i;
     st->tune_winner[level - 1] = best;
     st->cfg[level - 1] = c_choice[best];
+    if (host_cfg) {  // mapped pinned memory: the host reads it once an event after this kernel completes
+      host_cfg[level - 1] = c_choice[best];
+      __threadfence_system();
+    }
   }
 }
 
@@ -297,8 +301,8 @@ void launch_tune_level(const TunePlan& p, const void* field, int prec, const uin
 }
 
 void launch_tune_select(const TunePlan& p, int level, const double* berr, DevState* st, cudaStream_t s,
-                        int* launches) {
-  k_tune_select<<<1, 32, 0, s>>>(p.nb, level, berr, st);
+                        int* launches, uint8_t* host_cfg) {
+  k_tune_select<<<1, 32, 0, s>>>(p.nb, level, berr, st, host_cfg);
   (*launches)++;
 }
 
