@@ -73,6 +73,7 @@ class Clocks:
     def __init__(self, index: int):
         self.index = index
         self.samples = []
+        self.h = None
         self.stop = threading.Event()
         self.max_mhz = None
 
@@ -80,27 +81,37 @@ class Clocks:
         import pynvml
         h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
         self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        self.h = h
         while not self.stop.is_set():
-            try:
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((sm, rs))
-            except Exception:
-                pass
-            time.sleep(0.005)
+            self._sample()
+            self.ready.set()
+            time.sleep(0.002)
+
+    def _sample(self):
+        import pynvml
+        try:
+            sm = pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            self.samples.append((sm, rs))
+        except Exception:
+            pass
 
     def __enter__(self):
         try:
             import pynvml
             pynvml.nvmlInit()
+            self.ready = threading.Event()
             self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
-            time.sleep(0.02)
+            self.ready.wait(2.0)  # the poller is sampling before the timed region starts
+            self.samples.clear()
         except Exception:
             self.t = None
         return self
 
     def __exit__(self, *a):
+        if self.t and not self.samples and getattr(self, "h", None) is not None:
+            self._sample()  # a region shorter than one poll: sample at its end
         self.stop.set()
         if self.t:
             self.t.join(timeout=2)

@@ -39,8 +39,9 @@ constexpr int TY = 8, TZ = 32;
 constexpr int TZH = TZ + 4;  // z-source box z0-2 .. z0+TZ+1 (even start, 16-byte multiple)
 constexpr int T_THREADS = TY * 32;
 // targets per thread along x (per step: 16 was measured slower for every K on
-// B200 -- fewer resident blocks outweigh the amortised per-thread setup)
-constexpr __host__ __device__ int txof(int) { return 8; }
+// B200 -- fewer resident blocks outweigh the amortised per-thread setup; the
+// three-source step takes 4 so its three tiles leave room for 4 blocks / SM)
+constexpr __host__ __device__ int txof(int k) { return k == 3 ? 4 : 8; }
 // doubles per source tile slot: the largest of the x / y / z boxes
 constexpr __host__ __device__ int cmax(int a, int b) { return a > b ? a : b; }
 constexpr __host__ __device__ int slot_of(int tx) {
@@ -364,7 +365,7 @@ __device__ __forceinline__ void tp_block(const TPassArgs& A, const TMaps& M, int
 // by the other classes.
 template <typename T, bool DEC, int K, bool LINEAR, bool LV1, int C0 = -1, int C1 = -1, int C2 = -1,
           int TX = txof(K)>
-__global__ void __launch_bounds__(T_THREADS, C0 >= 0 ? (K == 3 ? 3 : 4) : 2) k_tpass(const __grid_constant__ TPassArgs A,
+__global__ void __launch_bounds__(T_THREADS, C0 >= 0 ? 4 : 2) k_tpass(const __grid_constant__ TPassArgs A,
                                                          const __grid_constant__ TMaps M) {
   extern __shared__ __align__(128) double tiles[];
   __shared__ unsigned shist[256];
