@@ -102,3 +102,28 @@ def test_forced_configs_match_oracle(oracle, dims, dt):
         rec = hb.reconstruct(qf, eb, cfg, dims=f.dims, ndim=f.ndim)
         ref = oracle.reconstruct(codes, oidx, oval, anchors, eb, list(cb), dims, vals.dtype)
         assert np.array_equal(rec.values.reshape(-1), ref.reshape(-1)), (dims, cb)
+
+
+def test_interleaved_calls_reuse_state_correctly(oracle):
+    """Context state carried between calls (resident compress tables, graph
+    replays, the shared arena, the in-stream archive copy into a caller's
+    device buffer) never changes an archive: interleave two shapes, both
+    modes, decompressions and a stage call, compare every archive with the
+    oracle's."""
+    import torch
+    va = synth.make("grf", (40, 56, 72), seed=3)
+    vb = synth.make("rough", (33, 48, 21), seed=4)
+    ref = {("a", "cr"): oracle.compress(va, "rel", 1e-3, "cr", 3), ("b", "tp"): oracle.compress(vb, "rel", 1e-3, "tp", 3)}
+    fields = {"a": hb.Field(torch.from_numpy(va).cuda()), "b": hb.Field(torch.from_numpy(vb).cuda())}
+    spec = hb.ErrorBoundSpec("rel", 1e-3)
+    bufs = {k: torch.full((hb.compress_bound(f.dims, 4),), 0xA5, dtype=torch.uint8, device="cuda")
+            for k, f in fields.items()}
+    for rnd in range(3):
+        for (k, mode) in (("a", "cr"), ("a", "cr"), ("b", "tp"), ("a", "cr"), ("b", "tp"), ("b", "tp")):
+            out = hb.compress_device(fields[k], spec, mode, out=bufs[k] if rnd % 2 else None)
+            assert out.cpu().numpy().tobytes() == ref[(k, mode)], (rnd, k, mode)
+            if rnd == 1:
+                back = hb.decompress_device(out, fields[k].dims, np.float32)
+                assert back.values.shape == fields[k].values.shape
+        hb.stages.huffman_encode(bytes(range(256)) * 3)
+    assert hb.compress(hb.Field(va), spec, "cr") == ref[("a", "cr")]
