@@ -336,10 +336,10 @@ __device__ __forceinline__ void tp_block(const TPassArgs& A, const TMaps& M, int
   mbar_wait(&bar, 0);
   if (live) {
     if (full)
-      tp_run<T, DEC, K, LINEAR, true, LV1>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb, two_eb, inv_two_eb, ocount,
+      tp_run<T, DEC, K, LINEAR, true, LV1, TX>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb, two_eb, inv_two_eb, ocount,
                                       shist, acc);
     else
-      tp_run<T, DEC, K, LINEAR, false, LV1>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb, two_eb, inv_two_eb,
+      tp_run<T, DEC, K, LINEAR, false, LV1, TX>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb, two_eb, inv_two_eb,
                                        ocount, shist, acc);
   }
   if (DEC && __any_sync(0xffffffffu, acc.nf) && zl == 0) raise_flag(A.st, F_NONFINITE);
