@@ -568,32 +568,41 @@ __global__ void __launch_bounds__(512) k_huff_build(DevState* st, unsigned long 
   }
   __syncthreads();
   // heapq on (freq, id) == two-queue merge: leaves in (freq, sym) order,
-  // internal nodes FIFO (ids ascending, freqs non-decreasing), leaf first on ties
+  // internal nodes FIFO (ids ascending, freqs non-decreasing), leaf first on
+  // ties.  One thread; the heads of both queues live in registers so an
+  // iteration waits on at most one shared load (the serial chain is the cost).
+  __shared__ unsigned long long sf[256];
+  if (t < np) sf[t] = f[sorted[t]];
+  __syncthreads();
   if (t == 0 && np > 1) {
     int li = 0, ih = 0;
-    unsigned long long fl = f[sorted[0]];
+    unsigned long long fl = sf[0], fi = 0;  // leaf head, internal head (valid while ih < m)
     for (int m = 0; m < np - 1; m++) {
       int pick0, pick1;
       unsigned long long p0, p1;
-      if (li < np && (ih >= m || fl <= ifreq[ih])) {
+      if (li < np && (ih >= m || fl <= fi)) {
         pick0 = sorted[li], p0 = fl;
         li++;
-        fl = li < np ? f[sorted[li]] : 0;
+        fl = li < np ? sf[li] : 0;
       } else {
-        pick0 = 256 + ih, p0 = ifreq[ih];
+        pick0 = 256 + ih, p0 = fi;
         ih++;
+        fi = ih < m ? ifreq[ih] : 0;
       }
-      if (li < np && (ih >= m || fl <= ifreq[ih])) {
+      if (li < np && (ih >= m || fl <= fi)) {
         pick1 = sorted[li], p1 = fl;
         li++;
-        fl = li < np ? f[sorted[li]] : 0;
+        fl = li < np ? sf[li] : 0;
       } else {
-        pick1 = 256 + ih, p1 = ifreq[ih];
+        pick1 = 256 + ih, p1 = fi;
         ih++;
+        fi = ih < m ? ifreq[ih] : 0;
       }
       parent[pick0] = 256 + m;
       parent[pick1] = 256 + m;
-      ifreq[m] = p0 + p1;
+      const unsigned long long nf = p0 + p1;
+      ifreq[m] = nf;
+      if (ih == m) fi = nf;  // the new node heads an empty internal queue
     }
   }
   __syncthreads();
