@@ -1269,6 +1269,11 @@ __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsi
                                                   HDTables* T, DevState* st) {
   __shared__ int ok_sh, cnt[257], maxlen_sh;
   __shared__ uint8_t len[256];
+  // shared copies of the canonical tables for the parallel LUT builds below
+  __shared__ unsigned long long s_first[64];
+  __shared__ int s_rank[64], s_count[64];
+  __shared__ uint8_t s_syms[256];
+  __shared__ uint16_t s_lut[1 << HD_K];
   const int t = threadIdx.x;
   if (t == 0) {
     T->ok = 0;
@@ -1335,17 +1340,18 @@ __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsi
     if (good) {
       unsigned long long next = 0;
       int prev = 0, r = 0;
-      for (int L = 0; L < 64; L++) T->first_rank[L] = -1, T->count[L] = 0, T->first_code[L] = 0;
+      for (int L = 0; L < 64; L++) s_rank[L] = -1, s_count[L] = 0, s_first[L] = 0;
       for (int L = 1; L <= maxlen; L++) {
         if (!cnt[L]) continue;
         next <<= (L - prev);
         prev = L;
-        T->first_rank[L] = r;
-        T->first_code[L] = next;
-        T->count[L] = cnt[L];
+        s_rank[L] = r;
+        s_first[L] = next;
+        s_count[L] = cnt[L];
         next += cnt[L];
         r += cnt[L];
       }
+      for (int L = 0; L < 64; L++) T->first_rank[L] = s_rank[L], T->count[L] = s_count[L], T->first_code[L] = s_first[L];
       T->maxlen = maxlen;
       T->K = maxlen < HD_K ? maxlen : HD_K;
       T->nsub = cdiv(T->nbits, HD_S);
@@ -1360,22 +1366,24 @@ __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsi
     for (int L = 1; L < len[t]; L++) r += cnt[L];
     for (int j = 0; j < t; j++) r += len[j] == len[t];
     T->syms[r] = (uint8_t)t;
+    s_syms[r] = (uint8_t)t;
   }
   __syncthreads();
-  const int K = T->K;
+  const int K = maxlen < HD_K ? maxlen : HD_K;
   for (int e = t; e < (1 << HD_K); e += 256) {
     uint16_t v = 0;
     if (e < (1 << K)) {
       for (int L = 1; L <= K; L++) {
-        if (!T->count[L]) continue;
+        if (!s_count[L]) continue;
         const unsigned long long c = (unsigned long long)e >> (K - L);
-        if (c >= T->first_code[L] && c - T->first_code[L] < (unsigned long long)T->count[L]) {
-          v = (uint16_t)((L << 8) | T->syms[T->first_rank[L] + (int)(c - T->first_code[L])]);
+        if (c >= s_first[L] && c - s_first[L] < (unsigned long long)s_count[L]) {
+          v = (uint16_t)((L << 8) | s_syms[s_rank[L] + (int)(c - s_first[L])]);
           break;
         }
       }
     }
     T->lut[e] = v;
+    s_lut[e] = v;
   }
   __syncthreads();
   // multi-symbol entries: greedy decode of the codewords wholly inside the window
@@ -1386,7 +1394,7 @@ __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsi
       while (n < 4) {
         const int rem = K - used;
         if (rem <= 0) break;
-        const uint16_t v = T->lut[((unsigned)e << used) & ((1u << K) - 1)];
+        const uint16_t v = s_lut[((unsigned)e << used) & ((1u << K) - 1)];
         const int L = v >> 8;
         if (!v || L > rem) break;
         packed |= (uint32_t)(v & 0xFF) << (8 * n);
@@ -1398,7 +1406,7 @@ __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsi
     T->mmeta[e] = (uint8_t)(n | (used << 3));
   }
   if (t == 0) {
-    T->run_sym = (T->count[1] > 0 && T->first_code[1] == 0) ? T->syms[T->first_rank[1]] : -1;
+    T->run_sym = (s_count[1] > 0 && s_first[1] == 0) ? s_syms[s_rank[1]] : -1;
     __threadfence();
     T->ok = 1;
   }
