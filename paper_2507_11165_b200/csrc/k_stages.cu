@@ -1842,25 +1842,32 @@ __global__ void __launch_bounds__(256) k_hd_pass(int p, const uint8_t* rec, cons
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) W.changed[p] = 1;
 }
 
-// exclusive scan of counts (decoupled look-back over 8192-entry tiles)
+// exclusive scan of counts (decoupled look-back over 2048-entry tiles staged
+// through shared memory: coalesced loads and stores)
+constexpr int HS_TILE = 2048;
 __global__ void __launch_bounds__(256) k_hd_scan(const HDTables* T, HDWork W, int fin, unsigned long long* lb,
                                                  DevState* st) {
   __shared__ unsigned long long sh[33];
   __shared__ unsigned long long tile_sh, base_sh;
+  __shared__ unsigned sc[HS_TILE];
+  __shared__ unsigned long long so[HS_TILE];
   if (!T->ok) return;
   const unsigned long long nsub = T->nsub;
-  const unsigned long long ntiles = cdiv(nsub, 8192);
+  const unsigned long long ntiles = cdiv(nsub, (unsigned long long)HS_TILE);
   const unsigned* c = W.c[fin];
   for (;;) {
     if (threadIdx.x == 0) tile_sh = atomicAdd(lb, 1ull);
     __syncthreads();
     const unsigned long long tile = tile_sh;
     if (tile >= ntiles) break;
-    const unsigned long long i0 = tile * 8192 + (unsigned long long)threadIdx.x * 32;
-    unsigned long long v[32], sum = 0;
+    const unsigned long long b0 = tile * HS_TILE;
+    for (int k = threadIdx.x; k < HS_TILE; k += blockDim.x) sc[k] = b0 + k < nsub ? c[b0 + k] : 0u;
+    __syncthreads();
+    unsigned v[8];
+    unsigned long long sum = 0;
 #pragma unroll
-    for (int k = 0; k < 32; k++) {
-      v[k] = i0 + k < nsub ? c[i0 + k] : 0;
+    for (int k = 0; k < 8; k++) {
+      v[k] = sc[threadIdx.x * 8 + k];
       sum += v[k];
     }
     unsigned long long total;
@@ -1872,11 +1879,13 @@ __global__ void __launch_bounds__(256) k_hd_scan(const HDTables* T, HDWork W, in
     __syncthreads();
     unsigned long long r = base_sh + ex;
 #pragma unroll
-    for (int k = 0; k < 32; k++)
-      if (i0 + k < nsub) {
-        W.off[i0 + k] = r;
-        r += v[k];
-      }
+    for (int k = 0; k < 8; k++) {
+      so[threadIdx.x * 8 + k] = r;
+      r += v[k];
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < HS_TILE; k += blockDim.x)
+      if (b0 + k < nsub) W.off[b0 + k] = so[k];
     if (tile == ntiles - 1 && threadIdx.x == 0) {
       const unsigned long long tot = base_sh + total;
       if (tot != T->nsym) raise_flag(st, F_STAGE, 160);
@@ -2134,7 +2143,7 @@ void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long*
   const int fin = 0;
   k_hd_serial<<<1, 1, 0, s>>>(hf_rec, T, W, fin);
   (*launches)++;
-  k_hd_scan<<<persist_grid(cdiv(nsub_max, 8192)), 256, 0, s>>>(T, W, fin, lb_ws, st);
+  k_hd_scan<<<persist_grid(cdiv(nsub_max, (unsigned long long)HS_TILE)), 256, 0, s>>>(T, W, fin, lb_ws, st);
   (*launches)++;
   k_hd_emit<<<g, 256, 0, s>>>(hf_rec, T, W, fin, seq, st);
   (*launches)++;
