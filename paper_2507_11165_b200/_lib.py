@@ -22,7 +22,7 @@ HB_OK, HB_EARG, HB_EFIELD, HB_EBOUND, HB_EARCHIVE, HB_ESTAGE, HB_ECUDA, HB_EUNSU
 
 _lib = None
 _lock = threading.Lock()
-_ctxs: dict = {}
+_tls = threading.local()
 
 
 class Info(C.Structure):
@@ -87,11 +87,39 @@ def current_device_and_stream():
     return 0, 0
 
 
+class _Contexts(dict):
+    """This thread's contexts, keyed by (device, stream).  Lives in a
+    threading.local, so when the thread exits (or release_contexts() runs)
+    every context is destroyed and its device arena, pinned staging, second
+    stream and recorded graphs are returned."""
+
+    def release(self):
+        L = _lib
+        while self:
+            _, c = self.popitem()
+            if L is not None:
+                L.hb_ctx_destroy(c)
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:  # interpreter shutdown
+            pass
+
+
+def _thread_contexts() -> _Contexts:
+    cs = getattr(_tls, "ctxs", None)
+    if cs is None:
+        cs = _tls.ctxs = _Contexts()
+    return cs
+
+
 def ctx():
-    """Context bound to torch's current device and stream (created on demand)."""
+    """Context bound to torch's current device and stream (created on demand,
+    one per thread: a context is single-stream and never shared)."""
     dev, stream = current_device_and_stream()
-    key = (dev, stream, threading.get_ident())
-    c = _ctxs.get(key)
+    cs = _thread_contexts()
+    c = cs.get((dev, stream))
     if c is None:
         L = lib()
         p = C.c_void_p()
@@ -99,8 +127,14 @@ def ctx():
         if rc != HB_OK:
             raise RuntimeError(f"hb_ctx_create failed (code {rc}): no usable CUDA device for the B200 path")
         c = p
-        _ctxs[key] = c
+        cs[(dev, stream)] = c
     return c
+
+
+def release_contexts():
+    """Destroy the calling thread's contexts now (device memory back to the
+    driver); the next call creates a fresh one."""
+    _thread_contexts().release()
 
 
 def raise_for(rc: int, c=None, what: str = ""):

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import struct
+import threading
 
 import numpy as np
 
@@ -39,7 +40,7 @@ def compress_bound(dims, precision: int) -> int:
     return n.value
 
 
-def _compress_into(field: Field, spec: ErrorBoundSpec, mode: str, out, cap: int):
+def _compress_call(field: Field, spec: ErrorBoundSpec, mode: str, out, cap: int):
     if mode not in _MODE_BYTE:
         raise ValueError(f"mode must be {MODE_CR!r} or {MODE_TP!r}, got {mode!r}")
     L, c = _lib.lib(), _lib.ctx()
@@ -49,35 +50,52 @@ def _compress_into(field: Field, spec: ErrorBoundSpec, mode: str, out, cap: int)
     rc = L.hb_compress(c, _lib.ptr(field.values), _prec(field), _lib.dims3(field.dims), field.ndim,
                        0 if spec.mode == "abs" else 1, float(spec.magnitude), _MODE_BYTE[mode], _lib.ptr(out), cap,
                        C.byref(olen), C.byref(eb), cfg)
+    return rc, c, olen.value
+
+
+def _compress_into(field: Field, spec: ErrorBoundSpec, mode: str, out, cap: int):
+    rc, c, n = _compress_call(field, spec, mode, out, cap)
     _lib.raise_for(rc, c)
-    return olen.value, eb.value, bytes(cfg)
+    return n
 
 
-_PINNED = {"buf": None}
+_STAGING = threading.local()
 
 
-def _pinned(cap: int):
-    """Reusable page-locked staging buffer for archive read-back."""
-    b = _PINNED["buf"]
+def _staging(cap: int):
+    """This thread's page-locked read-back buffer (ctypes releases the GIL
+    inside hb_compress, so concurrent callers must not share one)."""
+    b = getattr(_STAGING, "buf", None)
     if b is None or b.size < cap:
         try:
             import torch
             t = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
-            _PINNED["tensor"] = t
+            _STAGING.tensor = t  # keeps the pinned allocation alive with the thread
             b = t.numpy()
         except Exception:
             b = np.empty(cap, np.uint8)
-        _PINNED["buf"] = b
+        _STAGING.buf = b
     return b
 
 
 def compress(field: Field, spec: ErrorBoundSpec, mode: str = MODE_CR) -> bytes:
-    """Compress a field under the given error bound; returns archive bytes."""
+    """Compress a field under the given error bound; returns archive bytes.
+
+    The archive is staged in a per-thread pinned buffer sized for the common
+    case (raw field size + 64 KiB); an archive larger than that (outlier-heavy
+    fields) is re-run into a buffer of the exact length the first call
+    reported.  Reentrant: nothing is shared between threads."""
     if mode not in _MODE_BYTE:
         raise ValueError(f"mode must be {MODE_CR!r} or {MODE_TP!r}, got {mode!r}")
-    cap = compress_bound(field.dims, _prec(field))
-    out = _pinned(cap)
-    n, _, _ = _compress_into(field, spec, mode, out, cap)
+    bound = compress_bound(field.dims, _prec(field))
+    n_pts = int(np.prod(field.dims))
+    cap = min(bound, n_pts * _prec(field) + (1 << 16))
+    out = _staging(cap)
+    rc, c, n = _compress_call(field, spec, mode, out, cap)
+    if rc == _lib.HB_EARG and cap < n <= bound:
+        out = _staging(n)
+        rc, c, n = _compress_call(field, spec, mode, out, n)
+    _lib.raise_for(rc, c)
     return out[:n].tobytes()
 
 
@@ -87,21 +105,8 @@ def compress_device(field: Field, spec: ErrorBoundSpec, mode: str = MODE_CR, out
     cap = compress_bound(field.dims, _prec(field))
     if out is None or out.numel() < cap:
         out = torch.empty(cap, dtype=torch.uint8, device=field.values.device)
-    n, _, _ = _compress_into(field, spec, mode, out, cap)
+    n = _compress_into(field, spec, mode, out, cap)
     return out[:n]
-
-
-def _info(blob) -> "_lib.Info":
-    info = _lib.Info()
-    L = _lib.lib()
-    if _lib.is_cuda(blob):
-        return None
-    raw = bytes(blob) if not isinstance(blob, (bytes, np.ndarray)) else blob
-    arr = np.frombuffer(raw, np.uint8) if isinstance(raw, bytes) else raw
-    n = arr.size
-    keep = arr if n else np.zeros(1, np.uint8)
-    _lib.raise_for(L.hb_archive_info(_lib.ptr(keep), n, C.byref(info)), None, "archive")
-    return info
 
 
 def decompress(blob, out=None) -> Field:
@@ -130,35 +135,102 @@ def decompress(blob, out=None) -> Field:
     return Field._trusted(out, info.ndim)
 
 
-def decompress_device(archive, dims, dtype, ndim: int = 3, out=None):
-    """Device-resident decompress of a uint8 CUDA tensor archive into a CUDA tensor."""
+def _device_header(archive):
+    head = archive[:_FIXED.size].cpu().numpy().tobytes()
+    if len(head) < _FIXED.size:
+        raise ArchiveError("archive truncated in header")
+    f = _FIXED.unpack(head)
+    return (int(f[8]), int(f[9]), int(f[10])), (np.float32 if f[3] == 4 else np.float64), int(f[4])
+
+
+def decompress_device(archive, dims=None, dtype=None, ndim=None, out=None):
+    """Device-resident decompress of a uint8 CUDA tensor archive into a CUDA tensor.
+
+    dims / dtype / ndim default to the archive header's (dims or dtype left out
+    costs one 46-byte read-back); whatever the caller gives must match the
+    header, a mismatch raises ValueError instead of reinterpreting bytes."""
     import torch
+    if dims is None or dtype is None:
+        hd, ht, _ = _device_header(archive)
+        dims = hd if dims is None else dims
+        dtype = ht if dtype is None else dtype
+    dims = tuple(int(d) for d in dims)
+    dims3 = dims + (1,) if len(dims) == 2 else dims
     tdt = torch.float32 if np.dtype(dtype) == np.float32 else torch.float64
     if out is None:
-        out = torch.empty(tuple(dims), dtype=tdt, device=archive.device)
+        out = torch.empty(dims, dtype=tdt, device=archive.device)
     L, c = _lib.lib(), _lib.ctx()
-    rc = L.hb_decompress(c, _lib.ptr(archive), archive.numel(), _lib.ptr(out), out.numel() * out.element_size(), None)
+    info = _lib.Info()
+    rc = L.hb_decompress(c, _lib.ptr(archive), archive.numel(), _lib.ptr(out), out.numel() * out.element_size(),
+                         C.byref(info))
     _lib.raise_for(rc, c)
-    return Field._trusted(out, ndim)
+    got = (tuple(int(d) for d in info.dims), int(info.precision))
+    want = (dims3, np.dtype(dtype).itemsize)
+    if got != want or out.dtype != tdt or out.numel() != int(np.prod(dims3)) or \
+            (ndim is not None and int(ndim) != int(info.ndim)):
+        raise ValueError(f"archive holds dims {got[0]}, precision {got[1]}, ndim {info.ndim}; "
+                         f"caller asked for dims {dims3}, {np.dtype(dtype)}, ndim {ndim}")
+    return Field._trusted(out, int(info.ndim))
+
+
+def _parse_header(data: bytes, off: int = 0):
+    """archive.py:93-118: fixed header with the reference's checks and messages."""
+    if len(data) - off < _FIXED.size:
+        raise ArchiveError("archive truncated in header")
+    magic, version, mode_b, precision, ndim, stride, escape, cfg_raw, dx, dy, dz, eb = _FIXED.unpack_from(data, off)
+    if magic != MAGIC:
+        raise ArchiveError(f"bad magic {magic!r}")
+    if version != VERSION:
+        raise ArchiveError(f"unsupported archive version {version}")
+    if mode_b not in _MODE_NAME:
+        raise ArchiveError(f"unknown mode byte {mode_b}")
+    if precision not in (4, 8):
+        raise ArchiveError(f"unsupported precision {precision}")
+    if ndim not in (2, 3):
+        raise ArchiveError(f"unsupported ndim {ndim}")
+    if stride < 1 or stride > 16 or stride & (stride - 1):
+        raise ArchiveError(f"invalid anchor stride {stride}")
+    if escape not in (0, 1):
+        raise ArchiveError(f"invalid escape flag {escape}")
+    dims = (dx, dy, dz)
+    if any(d < 1 for d in dims):
+        raise ArchiveError(f"invalid dims {dims}")
+    if ndim == 2 and dz != 1:
+        raise ArchiveError("2D archive must carry a trailing dimension of 1")
+    if not (np.isfinite(eb) and eb > 0):
+        raise ArchiveError(f"invalid error bound {eb}")
+    config = InterpConfig.from_bytes(cfg_raw)
+    return _MODE_NAME[mode_b], precision, ndim, stride, bool(escape), config, dims, eb
 
 
 def section_sizes(blob: bytes) -> dict:
-    """Byte-level breakdown of an archive without decoding the stream (archive.py:174-200)."""
+    """Byte-level breakdown of an archive without decoding the stream
+    (archive.py:174-200): the same section walk, checks and messages as the
+    reference -- no anchor-count or trailing-byte validation here."""
     data = bytes(blob)
-    arr = np.frombuffer(data, np.uint8) if data else np.zeros(1, np.uint8)
-    info = _lib.Info()
-    rc = _lib.lib().hb_archive_info(_lib.ptr(arr), len(data), C.byref(info))
-    if rc:
-        raise ArchiveError("corrupt or truncated archive")
-    mode = _MODE_NAME[info.mode]
+    mode, precision, ndim, stride, escape, config, dims, eb = _parse_header(data)
+    off = _FIXED.size
+
+    def take(n, what):
+        nonlocal off
+        if len(data) - off < n:
+            raise ArchiveError(f"archive truncated in {what}")
+        off += n
+        return data[off - n:off]
+
+    anchor_count = _U64.unpack(take(8, "anchor count"))[0]
+    take(anchor_count * precision, "anchor values")
+    outlier_count = _U64.unpack(take(8, "outlier count"))[0]
+    take(outlier_count * (8 + precision), "outlier section")
+    stream_len = _U64.unpack(take(8, "stream length"))[0]
+    take(stream_len, "code stream")
     return {
-        "mode": mode, "precision": info.precision, "ndim": info.ndim,
-        "dims": tuple(int(d) for d in info.dims), "abs_eb": info.eb, "anchor_stride": info.stride,
-        "raw_escape": bool(info.escape), "header_bytes": _FIXED.size + 3 * 8,
-        "anchor_count": info.anchor_count, "anchor_bytes": info.anchor_count * info.precision,
-        "outlier_count": info.outlier_count, "outlier_bytes": info.outlier_count * (8 + info.precision),
-        "stream_bytes": info.stream_len, "total_bytes": len(data),
-        "huffman_table_bytes": 0 if (info.escape or mode != MODE_CR) else 256,
+        "mode": mode, "precision": precision, "ndim": ndim, "dims": dims, "abs_eb": eb,
+        "anchor_stride": stride, "raw_escape": escape, "header_bytes": _FIXED.size + 3 * 8,
+        "anchor_count": anchor_count, "anchor_bytes": anchor_count * precision,
+        "outlier_count": outlier_count, "outlier_bytes": outlier_count * (8 + precision),
+        "stream_bytes": stream_len, "total_bytes": len(data),
+        "huffman_table_bytes": 0 if (escape or mode != MODE_CR) else 256,
     }
 
 

@@ -1491,7 +1491,10 @@ int hb_stage_decode(hb_ctx* ctx, int stage, const void* in, size_t n, void* out,
   }
   const size_t o_a = L.take(capr + 512), o_b = L.take(capr + 512), o_c = L.take(capr + 512);
   const size_t o_bmd = L.take(1024);
-  const size_t hd_bytes = huffman_decode_ws_bytes(n + 64);
+  // the Huffman workspace is laid out for the max_payload handed to
+  // launch_huffman_decode_impl below: the record itself for a lone Huffman
+  // stage, the capacity-bounded intermediate record inside the CR pipeline
+  const size_t hd_bytes = huffman_decode_ws_bytes(stage == HB_PIPE_CR ? capr : n + 64);
   const size_t o_hd = L.take(hd_bytes);
   const unsigned long long lbn = lb_entries(capr, 256);
   const size_t o_lb = L.take(lbn * 8 * 12);

@@ -136,3 +136,48 @@ def test_device_archive_decompress_matches_host():
     out = hb.decompress_device(dev, c["input"].shape, c["input"].dtype)
     host = hb.decompress(blob)
     assert np.array_equal(out.values.cpu().numpy(), host.values)
+
+
+def test_decompress_device_checks_header():
+    """dims / dtype / ndim given by the caller must match the archive header
+    (a float64 request for an f32 archive is refused, not reinterpreted)."""
+    import torch
+    from paper_2507_11165_b200 import synth
+    vals = synth.make("grf", (20, 24, 28), seed=2)
+    arch = hb.compress_device(hb.Field(torch.from_numpy(vals).cuda()), hb.ErrorBoundSpec("rel", 1e-3))
+    r = hb.decompress_device(arch)
+    assert r.values.shape == (20, 24, 28) and r.values.dtype == torch.float32 and r.ndim == 3
+    with pytest.raises(ValueError):
+        hb.decompress_device(arch, (20, 24, 28), np.float64)
+    with pytest.raises(ValueError):
+        hb.decompress_device(arch, (20, 24, 28), np.float32, ndim=2)
+
+
+def test_concurrent_compress_threads(oracle):
+    """compress() is reentrant: threads compressing different
+    fields at once each get their own context and staging buffer."""
+    import threading
+    from paper_2507_11165_b200 import synth
+    fields = [synth.make(k, d, seed=s) for k, d, s in
+              (("grf", (40, 50, 60), 1), ("rough", (33, 48, 21), 2), ("gauss", (64, 64, 64), 3),
+               ("grf", (300, 400), 4))]
+    refs = [oracle.compress(v, "rel", 1e-3, "cr", v.ndim) for v in fields]
+    spec = hb.ErrorBoundSpec("rel", 1e-3)
+    errors = []
+
+    def work(i):
+        try:
+            for _ in range(4):
+                blob = hb.compress(hb.Field(fields[i], ndim=fields[i].ndim), spec, "cr")
+                if blob != refs[i]:
+                    errors.append(i)
+            hb._lib.release_contexts()
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(fields))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors

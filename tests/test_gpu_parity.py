@@ -111,3 +111,18 @@ def test_stage_records():
             assert st.rre_decode(c[f"rre{w}_{i}"].tobytes()) == data
             assert st.rze_encode(data, w) == c[f"rze{w}_{i}"].tobytes(), (i, w)
             assert st.rze_decode(c[f"rze{w}_{i}"].tobytes()) == data
+
+
+def test_fused_pipeline_decode_entry_points():
+    """hb_stage_decode(HB_PIPE_CR / HB_PIPE_TP) in one call: the CR pipeline's
+    Huffman workspace is laid out for the capacity-bounded intermediate record,
+    which for compressible inputs is far larger than the input record."""
+    from paper_2507_11165_b200 import stages as st
+    rng = np.random.default_rng(5)
+    cases = [bytes(200_000), (bytes([128]) * 90_000 + bytes(range(256)) * 40),
+             rng.integers(120, 137, 300_000).astype(np.uint8).tobytes(), b"x"]
+    for data in cases:
+        cr = st.pipeline_cr_encode(data)
+        tp = st.pipeline_tp_encode(data)
+        assert st._decode(st._PIPE_CR, cr, len(data) + 64) == data
+        assert st._decode(st._PIPE_TP, tp, len(data) + 64) == data

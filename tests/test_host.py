@@ -47,14 +47,30 @@ def test_archive_info_without_gpu():
         assert s["outlier_count"] == c["oidx"].size
         assert s["abs_eb"] == float(c["eb"])
         for cut in (0, 10, 45, 46, len(blob) // 2, len(blob) - 1):
-            with pytest.raises(hb.ArchiveError):
+            with pytest.raises(hb.ArchiveError, match="archive truncated in "):
                 hb.section_sizes(blob[:cut])
-        with pytest.raises(hb.ArchiveError):
-            hb.section_sizes(blob + b"\0")
+        # like the reference (archive.py:174-200) the walk ignores trailing bytes
+        assert hb.section_sizes(blob + b"\0")["total_bytes"] == len(blob) + 1
         bad = bytearray(blob)
         bad[0] ^= 0xFF
-        with pytest.raises(hb.ArchiveError):
+        with pytest.raises(hb.ArchiveError, match="bad magic"):
             hb.section_sizes(bytes(bad))
+
+
+def test_section_sizes_messages_match_reference():
+    """Messages observed from hibound.section_sizes on the affine 64^3 golden."""
+    blob = load_case("affine64_abs1e-3")["arch_cr"].tobytes()
+    expect = {0: "archive truncated in header", 45: "archive truncated in header",
+              46: "archive truncated in anchor count", len(blob) // 2: "archive truncated in anchor values"}
+    for cut, msg in expect.items():
+        with pytest.raises(hb.ArchiveError) as e:
+            hb.section_sizes(blob[:cut])
+        assert str(e.value) == msg
+    bad = bytearray(blob)
+    bad[0] ^= 0xFF
+    with pytest.raises(hb.ArchiveError) as e:
+        hb.section_sizes(bytes(bad))
+    assert str(e.value) == "bad magic b'\\xbcSZH'"
 
 
 def test_interp_config_bytes():
