@@ -64,6 +64,13 @@ int launch_level_pass_compress(const LevelGeom& g, const void* field, int prec, 
 int launch_level_pass_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
                                  const unsigned long long* ocount_dev, double* E, void* out, int prec, double* scr,
                                  DevState* st, cudaStream_t s, int cfg);
+// k_march.cu: a multidim 3D level in one launch (axis-0 march, rolling plane
+// window in shared memory).  Returns launches, 0 = not handled.
+int launch_level_march_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq,
+                                uint32_t* obm, DevState* st, cudaStream_t s, int cfg);
+int launch_level_march_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
+                                  const unsigned long long* ocount_dev, double* E, void* out, int prec, DevState* st,
+                                  cudaStream_t s, int cfg);
 void launch_copy_anchors_out(const uint8_t* anchors, int prec, unsigned long long n, void* out, DevState* st,
                              cudaStream_t s, int* launches);
 void launch_outliers_parse(const uint8_t* rec, int prec, unsigned long long count_max,

@@ -543,6 +543,12 @@ void level_kernel_smem_init() {
 
 void launch_level_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq, uint32_t* obm,
                            DevState* st, cudaStream_t s, int* launches, int cfg, double* scr) {
+  if (!getenv("HB_GENERIC_LEVELS")) {  // multidim 3D levels: one marching launch (k_march.cu)
+    if (const int n = launch_level_march_compress(g, field, prec, E, seq, obm, st, s, cfg)) {
+      *launches += n;
+      return;
+    }
+  }
   if (!getenv("HB_GENERIC_LEVELS")) {  // level 1 of 3D fields: TMA dependency passes (k_pass.cu)
     if (const int n = launch_level_pass_compress(g, field, prec, E, seq, obm, scr, st, s, cfg)) {
       *launches += n;
@@ -570,6 +576,12 @@ void launch_level_compress(const LevelGeom& g, const void* field, int prec, doub
 void launch_level_decompress(const LevelGeom& g, const uint8_t* seq, const uint64_t* oidx, const double* oval,
                              const unsigned long long* ocount_dev, double* E, void* out, int prec, DevState* st,
                              cudaStream_t s, int* launches, int cfg, double* scr) {
+  if (!getenv("HB_GENERIC_LEVELS")) {  // multidim 3D levels: one marching launch (k_march.cu)
+    if (const int n = launch_level_march_decompress(g, seq, oidx, oval, ocount_dev, E, out, prec, st, s, cfg)) {
+      *launches += n;
+      return;
+    }
+  }
   if (!getenv("HB_GENERIC_LEVELS")) {  // level 1 of 3D fields: TMA dependency passes (k_pass.cu)
     if (const int n = launch_level_pass_decompress(g, seq, oidx, oval, ocount_dev, E, out, prec, scr, st, s, cfg)) {
       *launches += n;
