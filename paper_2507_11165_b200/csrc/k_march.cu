@@ -187,40 +187,6 @@ struct PlaneCtx {
   long long ebase;  // E index of (P0, 0, 0) (levels >= 2)
 };
 
-// prediction of item (iy, iz) of class C (predictor.py:209-256): along x from
-// the four axis-0 source planes, along y / z from the in-plane sources
-template <class G, int C, bool LINEAR, bool FAST>
-__device__ __forceinline__ double predict(const LevelGeom& g, int xcls, int P1, int P2, int iy, int iz,
-                                          const double* x0, const double* x1, const double* x2, const double* x3,
-                                          const double* ys, const double* zs) {
-  using cg = CG<G, C>;
-  constexpr int K = (int)cg::xo + (int)cg::yo + (int)cg::zo;
-  constexpr int ICLS = LINEAR ? ST_MID : ST_CUBIC;
-  constexpr int jx = 0, jy = (int)cg::xo, jz = (int)cg::xo + (int)cg::yo;
-  const int e = cg::e(iy, iz);
-  double pv[3] = {0.0, 0.0, 0.0};
-  int ov[3] = {0, 0, 0};
-  if (cg::xo) {
-    const int c = FAST ? ICLS : xcls;
-    pv[jx] = apply_stencil(c, (FAST && LINEAR) ? 0.0 : x0[e], x1[e], x2[e], (FAST && LINEAR) ? 0.0 : x3[e]);
-    ov[jx] = stencil_order(c);
-  }
-  if (cg::yo) {  // rows iy .. iy+3 of the same-z-parity array with y even
-    const int c = FAST ? ICLS : classify(P1, g.D[1], 1, LINEAR);
-    const double* q0 = ys + e;
-    pv[jy] = apply_stencil(c, (FAST && LINEAR) ? 0.0 : q0[0], q0[cg::PITCH], q0[2 * cg::PITCH],
-                           (FAST && LINEAR) ? 0.0 : q0[3 * cg::PITCH]);
-    ov[jy] = stencil_order(c);
-  }
-  if (cg::zo) {  // items iz .. iz+3 of the even-z array, row iy
-    const int c = FAST ? ICLS : classify(P2, g.D[2], 1, LINEAR);
-    const double* q0 = zs + iy * G::EZP + iz + 1;
-    pv[jz] = apply_stencil(c, (FAST && LINEAR) ? 0.0 : q0[0], q0[1], q0[2], (FAST && LINEAR) ? 0.0 : q0[3]);
-    ov[jz] = stencil_order(c);
-  }
-  return K == 1 ? pv[0] : combine_axes(K, pv, ov);
-}
-
 // in-plane part of the Eq. 3 slot (ordering.py:68-84)
 template <int C>
 __device__ __forceinline__ int slot_item(const LevelGeom& g, int P1, int P2) {
@@ -230,59 +196,6 @@ __device__ __forceinline__ int slot_item(const LevelGeom& g, int P1, int P2) {
     if (!((C >> 1) & 1)) s -= (P2 + 1) >> 1;
   }
   return s;
-}
-
-// quantize (predictor.py:313-329) or replay (:397-411) one item; emit = the
-// code / output belongs to this CTA.  Returns the reconstruction.
-template <typename T, bool DEC, bool LV1, class G, int C>
-__device__ __forceinline__ double finish(const MarchArgs& A, const PlaneCtx& pc, int Y0, int Z0, int P1, int P2,
-                                         bool emit, double pred, const T* fs, int code_in, QC& q, unsigned* shist) {
-  const LevelGeom& g = A.g;
-  const int s = (int)g.s;
-  double rv;
-  if (!DEC) {
-    const T o = fs[(P1 - Y0 + 2) * G::FC + (P2 - Z0 + 4)];
-    const int code = quantize_fast<sizeof(T) == 4>((double)o, pred, q.eb, q.two_eb, q.inv, &rv);
-    if (emit) {
-      A.seq[pc.sbase + slot_item<C>(g, P1, P2)] = (uint8_t)code;
-      const unsigned d = (unsigned)code - 127u;
-      if (d < 3u) {
-        q.hp += 1ull << (21 * d);
-      } else {
-        atomicAdd(&shist[code], 1u);
-        if (code == 0) {
-          const unsigned lin = (unsigned)(pc.lbase + (P1 * (int)g.d[2] + P2) * s);
-          atomicOr(&A.obm[lin >> 5], 1u << (lin & 31));
-          q.bad |= !isfinite((double)o);
-        }
-      }
-      if (!LV1) A.E[pc.ebase + ((long long)P1 * (s >> 1)) * g.Ed[2] + (long long)P2 * (s >> 1)] = rv;
-    }
-  } else {
-    const int lin = pc.lbase + (P1 * (int)g.d[2] + P2) * s;
-    if (code_in != 0)
-      rv = dequantize(pred, q.two_eb, code_in);
-    else
-      rv = m_outlier(A.oidx, A.oval, (unsigned long long)(unsigned)lin, q.ocount, &q.bad);
-    if (emit) {
-      if (LV1) {
-        reinterpret_cast<T*>(A.out)[lin] = (T)rv;
-        q.nf |= !isfinite(rv);
-      } else {
-        A.E[pc.ebase + ((long long)P1 * (s >> 1)) * g.Ed[2] + (long long)P2 * (s >> 1)] = rv;
-      }
-    }
-  }
-  return rv;
-}
-
-// the code byte of item (iy, iz) of class C in plane pc (decompress prefetch)
-template <class G, int C>
-__device__ __forceinline__ int code_of(const MarchArgs& A, const PlaneCtx& pc, int Y0, int Z0, int iy, int iz) {
-  using cg = CG<G, C>;
-  const int P1 = Y0 + cg::py(iy), P2 = Z0 + cg::pz(iz);
-  if (!pc.live || !((unsigned)P1 < (unsigned)A.g.D[1] && (unsigned)P2 < (unsigned)A.g.D[2])) return 0;
-  return __ldg(A.seq + pc.sbase + slot_item<C>(A.g, P1, P2));
 }
 
 // Halo items (not owned by any thread's core mapping) of the even-axis
@@ -349,39 +262,108 @@ __device__ __forceinline__ void stage_F(const MarchArgs& A, int P0, int Y0, int 
   }
 }
 
-// One item of class C: coordinates, prediction, then (after every prediction
-// of the half-phase has been issued, so the shared-memory loads of all items
-// overlap) quantize / replay and the stores.
-template <typename T, bool DEC, bool LINEAR, bool LV1, class G, int C, bool FAST>
-struct Job {
-  using cg = CG<G, C>;
-  int iy, iz, P1, P2;
-  bool ok;
-  double pred;
-  __device__ __forceinline__ void init(const LevelGeom& g, int Y0, int Z0, int iy_, int iz_, bool live) {
-    iy = iy_, iz = iz_;
-    P1 = Y0 + cg::py(iy), P2 = Z0 + cg::pz(iz);
-    ok = live && (FAST || ((unsigned)P1 < (unsigned)g.D[1] && (unsigned)P2 < (unsigned)g.D[2]));
-  }
-  __device__ __forceinline__ void predict_(const LevelGeom& g, int xcls, const double* x0, const double* x1,
-                                           const double* x2, const double* x3, const double* ys, const double* zs) {
-    if (ok) pred = predict<G, C, LINEAR, FAST>(g, xcls, P1, P2, iy, iz, x0, x1, x2, x3, ys, zs);
-  }
-  __device__ __forceinline__ void finish_(const MarchArgs& A, const PlaneCtx& pc, int Y0, int Z0, bool core,
-                                          double* dst, const T* fs, int code, QC& q, unsigned* shist) {
-    if (!ok) return;
-    const double rv = finish<T, DEC, LV1, G, C>(A, pc, Y0, Z0, P1, P2, core && pc.owned, pred, fs, code, q, shist);
-    if (C != 7) dst[cg::e(iy, iz)] = rv;
-  }
-};
-
+// --------------------------------------------------------------- item bodies
 template <bool B>
 struct BT {
   static constexpr bool v = B;
 };
 
+// A thread's item of some class: where it lives in the class array (e), where
+// its y / z stencil sources start (ey: same layout, rows iy..iy+3; ez: the
+// even-z array, items iz..iz+3), its field value in the staged rectangle (f),
+// the in-plane parts of its Eq. 3 slot / element index / E index, and its
+// lattice coordinates (edge tiles classify and bound-check from them).
+struct ItemAt {
+  int e, ez, f, slot, lin, P1, P2;
+  long long eidx;
+};
+
+template <class G, int C>
+__device__ __forceinline__ ItemAt item_at(const LevelGeom& g, int Y0, int Z0, int iy, int iz) {
+  using cg = CG<G, C>;
+  ItemAt it;
+  it.P1 = Y0 + cg::py(iy), it.P2 = Z0 + cg::pz(iz);
+  it.e = cg::e(iy, iz);
+  it.ez = iy * G::EZP + iz + 1;
+  it.f = (it.P1 - Y0 + 2) * G::FC + (it.P2 - Z0 + 4);
+  it.slot = slot_item<C>(g, it.P1, it.P2);
+  const int s = (int)g.s;
+  it.lin = (it.P1 * (int)g.d[2] + it.P2) * s;
+  it.eidx = ((long long)it.P1 * (s >> 1)) * g.Ed[2] + (long long)it.P2 * (s >> 1);
+  return it;
+}
+
+// stencil along an in-plane axis (taps p[0], p[st], p[2st], p[3st]) or along
+// axis 0 (tap i from plane i at e)
+template <bool LINEAR, bool INT>
+__device__ __forceinline__ double st_in(const double* p, int st, int cls) {
+  const int c = INT ? (LINEAR ? ST_MID : ST_CUBIC) : cls;
+  return apply_stencil(c, (INT && LINEAR) ? 0.0 : p[0], p[st], p[2 * st], (INT && LINEAR) ? 0.0 : p[3 * st]);
+}
+template <bool LINEAR, bool INT>
+__device__ __forceinline__ double st_x(const double* a, const double* b, const double* c, const double* d, int e,
+                                       int cls) {
+  const int k = INT ? (LINEAR ? ST_MID : ST_CUBIC) : cls;
+  return apply_stencil(k, (INT && LINEAR) ? 0.0 : a[e], b[e], c[e], (INT && LINEAR) ? 0.0 : d[e]);
+}
+// multi-axis average (predictor.py:247-256); interior: every order is equal
+template <bool INT>
+__device__ __forceinline__ double comb2(double a, int oa, double b, int ob) {
+  if (INT) return __dmul_rn(__dadd_rn(__dadd_rn(0.0, a), b), 0.5);
+  const double p[2] = {a, b};
+  const int o[2] = {oa, ob};
+  return combine_axes(2, p, o);
+}
+template <bool INT>
+__device__ __forceinline__ double comb3(double a, int oa, double b, int ob, double c, int oc) {
+  if (INT) return __ddiv_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, a), b), c), 3.0);
+  const double p[3] = {a, b, c};
+  const int o[3] = {oa, ob, oc};
+  return combine_axes(3, p, o);
+}
+
+// quantize (predictor.py:313-329) / replay (:397-411) of one item and its
+// emission when the CTA owns it
+template <typename T, bool DEC, bool LV1>
+__device__ __forceinline__ double fin(const MarchArgs& A, double pred, const T* fs, int f, int code_in, int slot,
+                                      int lin, long long eidx, bool emit, QC& q, unsigned* shist) {
+  double rv;
+  if (!DEC) {
+    const T o = fs[f];
+    const int code = quantize_fast<sizeof(T) == 4>((double)o, pred, q.eb, q.two_eb, q.inv, &rv);
+    if (emit) {
+      A.seq[slot] = (uint8_t)code;
+      const unsigned d = (unsigned)code - 127u;
+      if (d < 3u) {
+        q.hp += 1ull << (21 * d);
+      } else {
+        atomicAdd(&shist[code], 1u);
+        if (code == 0) {
+          atomicOr(&A.obm[(unsigned)lin >> 5], 1u << (lin & 31));
+          q.bad |= !isfinite((double)o);
+        }
+      }
+      if (!LV1) A.E[eidx] = rv;
+    }
+  } else {
+    if (code_in != 0)
+      rv = dequantize(pred, q.two_eb, code_in);
+    else
+      rv = m_outlier(A.oidx, A.oval, (unsigned long long)(unsigned)lin, q.ocount, &q.bad);
+    if (emit) {
+      if (LV1) {
+        reinterpret_cast<T*>(A.out)[lin] = (T)rv;
+        q.nf |= !isfinite(rv);
+      } else {
+        A.E[eidx] = rv;
+      }
+    }
+  }
+  return rv;
+}
+
 template <typename T, bool DEC, bool LINEAR, bool LV1, int TY, int TZ>
-__global__ void __launch_bounds__(MT, DEC ? 3 : 3) k_march(const __grid_constant__ MarchArgs A) {
+__global__ void __launch_bounds__(MT, 2) k_march(const __grid_constant__ MarchArgs A) {
   using G = MG<TY, TZ, DEC ? 0 : sizeof(T)>;
   static_assert(G::HY * G::HZ == MT, "one core item per class per thread");
   extern __shared__ __align__(128) double sm[];
@@ -407,25 +389,33 @@ __global__ void __launch_bounds__(MT, DEC ? 3 : 3) k_march(const __grid_constant
   }
   __syncthreads();
   const bool yzint = Y0 >= 2 && Y0 + TY + 2 < g.D[1] && Z0 >= 2 && Z0 + TZ + 2 < g.D[2];
-  // this thread's halo items: half 1 deals [c2 | c4 | c1] margins from
-  // thread 0, half 2 [c3 | c5] from the thread after the last half-1 item
+  // this thread's core items (one per class) and halo items (at most one per
+  // half-phase: half 1 deals the [c2 | c4 | c1] margins from thread 0, half 2
+  // the [c3 | c5] margins from the thread after the last half-1 item)
+  const ItemAt i1 = item_at<G, 1>(g, Y0, Z0, row + 1, tz + 1), i2 = item_at<G, 2>(g, Y0, Z0, row, tz + 1),
+               i3 = item_at<G, 3>(g, Y0, Z0, row, tz + 1), i4 = item_at<G, 4>(g, Y0, Z0, row + 1, tz),
+               i5 = item_at<G, 5>(g, Y0, Z0, row + 1, tz), i6 = item_at<G, 6>(g, Y0, Z0, row, tz),
+               i7 = item_at<G, 7>(g, Y0, Z0, row, tz);
   constexpr int NH2 = 3 * G::HY, NH4 = 3 * G::HZ, NH1 = 3 * G::EZ + 3 * G::HY;
   constexpr int NHA = NH2 + NH4 + NH1, NHB = NH2 + NH4;
   static_assert(NHA <= MT && NHB <= MT, "one halo item per thread and half");
-  int ha = (int)threadIdx.x, hb = (int)threadIdx.x - NHA;
-  if (hb < 0) hb += MT;
-  int hcA = 0, hyA = 0, hzA = 0, hcB = 0, hyB = 0, hzB = 0;
-  if (ha < NH2) {
-    hcA = 2, halo_item<G, 2>(ha, hyA, hzA);
-  } else if (ha < NH2 + NH4) {
-    hcA = 4, halo_item<G, 4>(ha - NH2, hyA, hzA);
-  } else if (ha < NHA) {
-    hcA = 1, halo_item<G, 1>(ha - NH2 - NH4, hyA, hzA);
-  }
-  if (hb < NH2) {
-    hcB = 3, halo_item<G, 3>(hb, hyB, hzB);
-  } else if (hb < NHB) {
-    hcB = 5, halo_item<G, 5>(hb - NH2, hyB, hzB);
+  int hcA = 0, hcB = 0;
+  ItemAt hA{}, hB{};
+  {
+    int ha = (int)threadIdx.x, hb = (int)threadIdx.x - NHA, iy = 0, iz = 0;
+    if (hb < 0) hb += MT;
+    if (ha < NH2) {
+      halo_item<G, 2>(ha, iy, iz), hcA = 2, hA = item_at<G, 2>(g, Y0, Z0, iy, iz);
+    } else if (ha < NH2 + NH4) {
+      halo_item<G, 4>(ha - NH2, iy, iz), hcA = 4, hA = item_at<G, 4>(g, Y0, Z0, iy, iz);
+    } else if (ha < NHA) {
+      halo_item<G, 1>(ha - NH2 - NH4, iy, iz), hcA = 1, hA = item_at<G, 1>(g, Y0, Z0, iy, iz);
+    }
+    if (hb < NH2) {
+      halo_item<G, 3>(hb, iy, iz), hcB = 3, hB = item_at<G, 3>(g, Y0, Z0, iy, iz);
+    } else if (hb < NHB) {
+      halo_item<G, 5>(hb - NH2, iy, iz), hcB = 5, hB = item_at<G, 5>(g, Y0, Z0, iy, iz);
+    }
   }
   double* const sE = sm + G::oE;
   double* const sC2 = sm + G::oC2;
@@ -438,42 +428,32 @@ __global__ void __launch_bounds__(MT, DEC ? 3 : 3) k_march(const __grid_constant
   T* const sFo = sFe + G::RFE * G::SF;               // odd planes: slot m % RFO
   const int D1 = (int)g.D[1], D2 = (int)g.D[2], eyez = (int)g.eyez, pre = (int)g.prefix;
   const int plane = (int)(g.d[1] * g.d[2]) * (int)g.s;
-  auto ctx = [&](int P0, bool owned, bool live) {
-    PlaneCtx c;
-    c.P0 = P0;
-    c.owned = owned;
-    c.live = live;
-    c.xcls = (P0 & 1) ? classify(P0, g.D[0], 1, LINEAR) : 0;
-    c.sbase = pre + P0 * D1 * D2 - ((P0 + 1) >> 1) * eyez;
-    c.lbase = P0 * plane;
-    c.ebase = LV1 ? 0 : ((long long)P0 * (g.s >> 1)) * g.Ed[1] * g.Ed[2];
-    return c;
+  const long long eplane = LV1 ? 0 : (g.s >> 1) * g.Ed[1] * g.Ed[2];
+  auto sbase = [&](int P0) { return pre + P0 * D1 * D2 - ((P0 + 1) >> 1) * eyez; };
+  auto elive = [&](int j) { return j >= 0 && j < A.nep && j >= js - 1 && j <= je + 1; };
+  auto olive = [&](int m) { return m >= js && m < je && m < A.nop; };
+  auto code_at = [&](bool live, int P0, const ItemAt& it, bool edge) -> int {
+    if (!live || (edge && !((unsigned)it.P1 < (unsigned)D1 && (unsigned)it.P2 < (unsigned)D2))) return 0;
+    return __ldg(A.seq + sbase(P0) + it.slot);
   };
-  auto even_ctx = [&](int j) { return ctx(2 * j, j >= js && j < je, j >= 0 && j < A.nep && j >= js - 1 && j <= je + 1); };
-  auto odd_ctx = [&](int m) { return ctx(2 * m + 1, true, m >= js && m < je && m < A.nop); };
   // decompress: the code bytes of the next phase, prefetched a phase ahead
   int c2 = 0, c4 = 0, c1 = 0, c7 = 0, c6 = 0, c3 = 0, c5 = 0, cA = 0, cB = 0;
   auto prefetch_codes = [&](int k) {
     if (!DEC) return;
-    const PlaneCtx pe = even_ctx(k), p1 = odd_ctx(k - 2), p7 = odd_ctx(k - 3);
-    c2 = code_of<G, 2>(A, pe, Y0, Z0, row, tz + 1);
-    c4 = code_of<G, 4>(A, pe, Y0, Z0, row + 1, tz);
-    c6 = code_of<G, 6>(A, pe, Y0, Z0, row, tz);
-    c1 = code_of<G, 1>(A, p1, Y0, Z0, row + 1, tz + 1);
-    c3 = code_of<G, 3>(A, p1, Y0, Z0, row, tz + 1);
-    c5 = code_of<G, 5>(A, p1, Y0, Z0, row + 1, tz);
-    c7 = code_of<G, 7>(A, p7, Y0, Z0, row, tz);
-    cA = hcA == 2 ? code_of<G, 2>(A, pe, Y0, Z0, hyA, hzA)
-                  : (hcA == 4 ? code_of<G, 4>(A, pe, Y0, Z0, hyA, hzA)
-                              : (hcA == 1 ? code_of<G, 1>(A, p1, Y0, Z0, hyA, hzA) : 0));
-    cB = hcB == 3 ? code_of<G, 3>(A, p1, Y0, Z0, hyB, hzB) : (hcB == 5 ? code_of<G, 5>(A, p1, Y0, Z0, hyB, hzB) : 0);
+    const bool le = elive(k), l1 = olive(k - 2), l7 = olive(k - 3), ed = !yzint;
+    const int Pe = 2 * k, P1 = 2 * (k - 2) + 1, P7 = 2 * (k - 3) + 1;
+    c2 = code_at(le, Pe, i2, ed), c4 = code_at(le, Pe, i4, ed), c6 = code_at(le, Pe, i6, ed);
+    c1 = code_at(l1, P1, i1, ed), c3 = code_at(l1, P1, i3, ed), c5 = code_at(l1, P1, i5, ed);
+    c7 = code_at(l7, P7, i7, ed);
+    cA = code_at(hcA == 1 ? l1 : (hcA != 0 && le), hcA == 1 ? P1 : Pe, hA, true);
+    cB = code_at(hcB != 0 && l1, P1, hB, true);
   };
   unsigned phase = 0;
   constexpr int ME = G::RE - 1, MC = G::RC - 1;
   auto stage = [&](int k) {  // the TMA / cp.async inputs of phase k
     if (k <= je + 1) stage_E<G>(A, k, Y0, Z0, sE + (k & ME) * G::SE, &bar);
-    if (!DEC && even_ctx(k).live) stage_F<T, G>(A, 2 * k, Y0, Z0, sFe + (k & (G::RFE - 1)) * G::SF, &bar);
-    if (!DEC && odd_ctx(k - 2).live)
+    if (!DEC && elive(k)) stage_F<T, G>(A, 2 * k, Y0, Z0, sFe + (k & (G::RFE - 1)) * G::SF, &bar);
+    if (!DEC && olive(k - 2))
       stage_F<T, G>(A, 2 * (k - 2) + 1, Y0, Z0, sFo + ((k - 2) & (G::RFO - 1)) * G::SF, &bar);
     if (threadIdx.x == 0) mbar_arrive(&bar);
     cp_commit();
@@ -486,10 +466,16 @@ __global__ void __launch_bounds__(MT, DEC ? 3 : 3) k_march(const __grid_constant
   __syncthreads();
   for (int k = js - 1; k <= je + 2; k++) {
     const int m1 = k - 2, m7 = k - 3;  // odd planes of c1/c3/c5 and of c7
-    const PlaneCtx pe = even_ctx(k), p1 = odd_ctx(m1), p7 = odd_ctx(m7);
-    // half-phase variant: every item of the tile has complete cubic / linear
-    // stencils along every axis (no per-item validity or classification)
-    const bool fast = yzint && 2 * m7 + 1 >= 3 && 2 * m1 + 4 < g.D[0];
+    const bool le = elive(k), l1 = olive(m1), l7 = olive(m7);
+    const bool oe = k >= js && k < je;  // even plane k is owned
+    const int Pe = 2 * k, P1 = 2 * m1 + 1, P7 = 2 * m7 + 1;
+    const int sbE = sbase(Pe), sb1 = sbase(P1), sb7 = sbase(P7);
+    const int lbE = Pe * plane, lb1 = P1 * plane, lb7 = P7 * plane;
+    const long long ebE = Pe * eplane, eb1 = P1 * eplane, eb7 = P7 * eplane;
+    const int x1c = classify(P1, g.D[0], 1, LINEAR), x7c = classify(P7, g.D[0], 1, LINEAR);
+    // interior phase: every item of the tile has complete cubic / linear
+    // stencils along every axis (no per-item bounds or classification)
+    const bool fast = LV1 && yzint && P7 >= 3 && P1 + 3 < g.D[0];
     const double* Ek = sE + (k & ME) * G::SE;
     const T* fe = sFe + (k & (G::RFE - 1)) * G::SF;
     const T* f1 = sFo + (m1 & (G::RFO - 1)) * G::SF;
@@ -499,93 +485,356 @@ __global__ void __launch_bounds__(MT, DEC ? 3 : 3) k_march(const __grid_constant
     double* c6k = sC6 + (k & MC) * G::S6;
     const int k2 = c2, k4 = c4, k1 = c1, k7 = c7, k6 = c6, k3 = c3, k5 = c5, kA = cA, kB = cB;
     if (DEC) prefetch_codes(k + 1);
-    // ---- half 1: c2, c4 of plane k | c1 of odd m1 | c7 of odd m7 (| E points of plane k on decompress)
-    auto half1 = [&](auto F) {
-      constexpr bool FA = decltype(F)::v;
-      Job<T, DEC, LINEAR, LV1, G, 2, FA> j2, h2;
-      Job<T, DEC, LINEAR, LV1, G, 4, FA> j4, h4;
-      Job<T, DEC, LINEAR, LV1, G, 1, FA> j1, h1;
-      Job<T, DEC, LINEAR, LV1, G, 7, FA> j7;
-      j2.init(g, Y0, Z0, row, tz + 1, pe.live);
-      j4.init(g, Y0, Z0, row + 1, tz, pe.live);
-      j1.init(g, Y0, Z0, row + 1, tz + 1, p1.live);
-      j7.init(g, Y0, Z0, row, tz, p7.live);
-      h2.init(g, Y0, Z0, hyA, hzA, pe.live && hcA == 2);
-      h4.init(g, Y0, Z0, hyA, hzA, pe.live && hcA == 4);
-      h1.init(g, Y0, Z0, hyA, hzA, p1.live && hcA == 1);
-      const double* e0 = sE + ((m1 - 1) & ME) * G::SE;
-      const double* e1 = sE + (m1 & ME) * G::SE;
-      const double* e2 = sE + ((m1 + 1) & ME) * G::SE;
-      const double* e3 = sE + ((m1 + 2) & ME) * G::SE;
-      const double* s0 = sC6 + ((m7 - 1) & MC) * G::S6;
-      const double* s1 = sC6 + (m7 & MC) * G::S6;
-      const double* s2 = sC6 + ((m7 + 1) & MC) * G::S6;
-      const double* s3 = sC6 + ((m7 + 2) & MC) * G::S6;
-      j2.predict_(g, 0, 0, 0, 0, 0, Ek, 0);
-      j4.predict_(g, 0, 0, 0, 0, 0, 0, Ek);
-      j1.predict_(g, p1.xcls, e0, e1, e2, e3, 0, 0);
-      j7.predict_(g, p7.xcls, s0, s1, s2, s3, sC5, sC3);
-      h2.predict_(g, 0, 0, 0, 0, 0, Ek, 0);
-      h4.predict_(g, 0, 0, 0, 0, 0, 0, Ek);
-      h1.predict_(g, p1.xcls, e0, e1, e2, e3, 0, 0);
-      j2.finish_(A, pe, Y0, Z0, true, c2k, fe, k2, q, shist);
-      j4.finish_(A, pe, Y0, Z0, true, c4k, fe, k4, q, shist);
-      j1.finish_(A, p1, Y0, Z0, true, sC1, f1, k1, q, shist);
-      j7.finish_(A, p7, Y0, Z0, true, nullptr, f7, k7, q, shist);
-      h2.finish_(A, pe, Y0, Z0, false, c2k, fe, kA, q, shist);
-      h4.finish_(A, pe, Y0, Z0, false, c4k, fe, kA, q, shist);
-      h1.finish_(A, p1, Y0, Z0, false, sC1, f1, kA, q, shist);
-    };
-    if (fast)
-      half1(BT<true>{});
-    else
-      half1(BT<false>{});
-    if (DEC && LV1 && pe.live && pe.owned) {  // the 2-lattice points of plane k are outputs too
-      const int P1 = Y0 + 2 * row, P2 = Z0 + 2 * tz;
-      if (P1 < D1 && P2 < D2) {
-        const double v = Ek[(row + 1) * G::EZP + tz + 2];
-        reinterpret_cast<T*>(A.out)[pe.lbase + P1 * (int)g.d[2] + P2] = (T)v;
-        q.nf |= !isfinite(v);
+    auto phase_body = [&](auto F) {
+      constexpr bool I = decltype(F)::v;  // interior
+      auto ok = [&](const ItemAt& it) {
+        return I || ((unsigned)it.P1 < (unsigned)D1 && (unsigned)it.P2 < (unsigned)D2);
+      };
+      auto cy = [&](const ItemAt& it) { return I ? 0 : classify(it.P1, g.D[1], 1, LINEAR); };
+      auto cz = [&](const ItemAt& it) { return I ? 0 : classify(it.P2, g.D[2], 1, LINEAR); };
+      auto od = [&](int c) { return I ? (LINEAR ? 2 : 4) : stencil_order(c); };
+      // ---- half 1: c2, c4 of plane k | c1 of odd m1 | c7 of odd m7
+      {
+        const double* e0 = sE + ((m1 - 1) & ME) * G::SE;
+        const double* e1 = sE + (m1 & ME) * G::SE;
+        const double* e2 = sE + ((m1 + 1) & ME) * G::SE;
+        const double* e3 = sE + ((m1 + 2) & ME) * G::SE;
+        const double* s0 = sC6 + ((m7 - 1) & MC) * G::S6;
+        const double* s1 = sC6 + (m7 & MC) * G::S6;
+        const double* s2 = sC6 + ((m7 + 1) & MC) * G::S6;
+        const double* s3 = sC6 + ((m7 + 2) & MC) * G::S6;
+        const bool v2 = le && ok(i2), v4 = le && ok(i4), v1 = l1 && ok(i1), v7 = l7 && ok(i7);
+        double p2 = 0, p4 = 0, p1 = 0, p7 = 0;
+        if (v2) p2 = st_in<LINEAR, I>(Ek + i2.e, G::EZP, cy(i2));
+        if (v4) p4 = st_in<LINEAR, I>(Ek + i4.ez, 1, cz(i4));
+        if (v1) p1 = st_x<LINEAR, I>(e0, e1, e2, e3, i1.e, x1c);
+        if (v7) {
+          const int a = x7c, b = cy(i7), c = cz(i7);
+          p7 = comb3<I>(st_x<LINEAR, I>(s0, s1, s2, s3, i7.e, a), od(a), st_in<LINEAR, I>(sC5 + i7.e, G::HZ, b), od(b),
+                        st_in<LINEAR, I>(sC3 + i7.ez, 1, c), od(c));
+        }
+        if (v2) c2k[i2.e] = fin<T, DEC, LV1>(A, p2, fe, i2.f, k2, sbE + i2.slot, lbE + i2.lin, ebE + i2.eidx, oe, q, shist);
+        if (v4) c4k[i4.e] = fin<T, DEC, LV1>(A, p4, fe, i4.f, k4, sbE + i4.slot, lbE + i4.lin, ebE + i4.eidx, oe, q, shist);
+        if (v1) sC1[i1.e] = fin<T, DEC, LV1>(A, p1, f1, i1.f, k1, sb1 + i1.slot, lb1 + i1.lin, eb1 + i1.eidx, true, q, shist);
+        if (v7) fin<T, DEC, LV1>(A, p7, f7, i7.f, k7, sb7 + i7.slot, lb7 + i7.lin, eb7 + i7.eidx, true, q, shist);
+        // halo item of half 1
+        if (hcA == 2 && le && ok(hA)) {
+          c2k[hA.e] = fin<T, DEC, LV1>(A, st_in<LINEAR, I>(Ek + hA.e, G::EZP, cy(hA)), fe, hA.f, kA, 0, lbE + hA.lin, 0, false, q, shist);
+        } else if (hcA == 4 && le && ok(hA)) {
+          c4k[hA.e] = fin<T, DEC, LV1>(A, st_in<LINEAR, I>(Ek + hA.ez, 1, cz(hA)), fe, hA.f, kA, 0, lbE + hA.lin, 0, false, q, shist);
+        } else if (hcA == 1 && l1 && ok(hA)) {
+          sC1[hA.e] = fin<T, DEC, LV1>(A, st_x<LINEAR, I>(e0, e1, e2, e3, hA.e, x1c), f1, hA.f, kA, 0, lb1 + hA.lin, 0,
+                                       false, q, shist);
+        }
+        if (DEC && LV1 && le && oe) {  // the 2-lattice points of plane k are outputs too
+          if (ok(i1)) {
+            const double v = Ek[i1.e];
+            reinterpret_cast<T*>(A.out)[lbE + i1.lin] = (T)v;
+            q.nf |= !isfinite(v);
+          }
+        }
       }
-    }
-    __syncthreads();
-    // the inputs of phase k+1 land in the slots of planes k-3 (E, odd field)
-    // and k-1 (even field), free from here on
-    stage(k + 1);
-    // ---- half 2: c6 of plane k | c3, c5 of odd m1
-    auto half2 = [&](auto F) {
-      constexpr bool FA = decltype(F)::v;
-      Job<T, DEC, LINEAR, LV1, G, 6, FA> j6;
-      Job<T, DEC, LINEAR, LV1, G, 3, FA> j3, h3;
-      Job<T, DEC, LINEAR, LV1, G, 5, FA> j5, h5;
-      j6.init(g, Y0, Z0, row, tz, pe.live);
-      j3.init(g, Y0, Z0, row, tz + 1, p1.live);
-      j5.init(g, Y0, Z0, row + 1, tz, p1.live);
-      h3.init(g, Y0, Z0, hyB, hzB, p1.live && hcB == 3);
-      h5.init(g, Y0, Z0, hyB, hzB, p1.live && hcB == 5);
-      const double* b0 = sC2 + ((m1 - 1) & MC) * G::S2;
-      const double* b1 = sC2 + (m1 & MC) * G::S2;
-      const double* b2 = sC2 + ((m1 + 1) & MC) * G::S2;
-      const double* b3 = sC2 + ((m1 + 2) & MC) * G::S2;
-      const double* d0 = sC4 + ((m1 - 1) & MC) * G::S4;
-      const double* d1 = sC4 + (m1 & MC) * G::S4;
-      const double* d2 = sC4 + ((m1 + 1) & MC) * G::S4;
-      const double* d3 = sC4 + ((m1 + 2) & MC) * G::S4;
-      j6.predict_(g, 0, 0, 0, 0, 0, c4k, c2k);
-      j3.predict_(g, p1.xcls, b0, b1, b2, b3, sC1, 0);
-      j5.predict_(g, p1.xcls, d0, d1, d2, d3, 0, sC1);
-      h3.predict_(g, p1.xcls, b0, b1, b2, b3, sC1, 0);
-      h5.predict_(g, p1.xcls, d0, d1, d2, d3, 0, sC1);
-      j6.finish_(A, pe, Y0, Z0, true, c6k, fe, k6, q, shist);
-      j3.finish_(A, p1, Y0, Z0, true, sC3, f1, k3, q, shist);
-      j5.finish_(A, p1, Y0, Z0, true, sC5, f1, k5, q, shist);
-      h3.finish_(A, p1, Y0, Z0, false, sC3, f1, kB, q, shist);
-      h5.finish_(A, p1, Y0, Z0, false, sC5, f1, kB, q, shist);
+      __syncthreads();
+      // the inputs of phase k+1 land in the slots of planes k-3 (E, odd
+      // field) and k-1 (even field), free from here on
+      stage(k + 1);
+      // ---- half 2: c6 of plane k | c3, c5 of odd m1
+      {
+        const double* b0 = sC2 + ((m1 - 1) & MC) * G::S2;
+        const double* b1 = sC2 + (m1 & MC) * G::S2;
+        const double* b2 = sC2 + ((m1 + 1) & MC) * G::S2;
+        const double* b3 = sC2 + ((m1 + 2) & MC) * G::S2;
+        const double* d0 = sC4 + ((m1 - 1) & MC) * G::S4;
+        const double* d1 = sC4 + (m1 & MC) * G::S4;
+        const double* d2 = sC4 + ((m1 + 1) & MC) * G::S4;
+        const double* d3 = sC4 + ((m1 + 2) & MC) * G::S4;
+        const bool v6 = le && ok(i6), v3 = l1 && ok(i3), v5 = l1 && ok(i5);
+        double p6 = 0, p3 = 0, p5 = 0;
+        if (v6) {
+          const int b = cy(i6), c = cz(i6);
+          p6 = comb2<I>(st_in<LINEAR, I>(c4k + i6.e, G::HZ, b), od(b), st_in<LINEAR, I>(c2k + i6.ez, 1, c), od(c));
+        }
+        if (v3) {
+          const int b = cy(i3);
+          p3 = comb2<I>(st_x<LINEAR, I>(b0, b1, b2, b3, i3.e, x1c), od(x1c), st_in<LINEAR, I>(sC1 + i3.e, G::EZP, b),
+                        od(b));
+        }
+        if (v5) {
+          const int c = cz(i5);
+          p5 = comb2<I>(st_x<LINEAR, I>(d0, d1, d2, d3, i5.e, x1c), od(x1c), st_in<LINEAR, I>(sC1 + i5.ez, 1, c), od(c));
+        }
+        if (v6) c6k[i6.e] = fin<T, DEC, LV1>(A, p6, fe, i6.f, k6, sbE + i6.slot, lbE + i6.lin, ebE + i6.eidx, oe, q, shist);
+        if (v3) sC3[i3.e] = fin<T, DEC, LV1>(A, p3, f1, i3.f, k3, sb1 + i3.slot, lb1 + i3.lin, eb1 + i3.eidx, true, q, shist);
+        if (v5) sC5[i5.e] = fin<T, DEC, LV1>(A, p5, f1, i5.f, k5, sb1 + i5.slot, lb1 + i5.lin, eb1 + i5.eidx, true, q, shist);
+        if (hcB == 3 && l1 && ok(hB)) {
+          const int b = cy(hB);
+          sC3[hB.e] = fin<T, DEC, LV1>(A,
+                                       comb2<I>(st_x<LINEAR, I>(b0, b1, b2, b3, hB.e, x1c), od(x1c),
+                                                st_in<LINEAR, I>(sC1 + hB.e, G::EZP, b), od(b)),
+                                       f1, hB.f, kB, 0, lb1 + hB.lin, 0, false, q, shist);
+        } else if (hcB == 5 && l1 && ok(hB)) {
+          const int c = cz(hB);
+          sC5[hB.e] = fin<T, DEC, LV1>(A,
+                                       comb2<I>(st_x<LINEAR, I>(d0, d1, d2, d3, hB.e, x1c), od(x1c),
+                                                st_in<LINEAR, I>(sC1 + hB.ez, 1, c), od(c)),
+                                       f1, hB.f, kB, 0, lb1 + hB.lin, 0, false, q, shist);
+        }
+      }
+    };
+    // Interior phase (every stencil of the tile complete): the items of each
+    // half go through prediction, quantization / replay and stores as one
+    // batch, written breadth-first (each step for every item before the next
+    // step) so the FP64 dependency chains of different items interleave; the
+    // rare paths (exact-division quantizer fallback, histogram bins other
+    // than 127..129, outliers) are deferred behind one branch.  Planes that
+    // are not live are computed on stale shared memory and their stores
+    // predicated off.
+    auto fast_body = [&]() {
+      constexpr double W0 = LINEAR ? 0.0 : -0.0625, W1 = LINEAR ? 0.5 : 0.5625;
+      // NG stencil groups of 4 taps -> NG one-axis predictions, breadth-first
+      auto stencils = [&](auto& tp, auto& res, int ng) {
+#pragma unroll
+        for (int g_ = 0; g_ < 7; g_++) {
+          if (g_ >= ng) break;
+          if (LINEAR) {
+            res[g_] = __dadd_rn(__dmul_rn(tp[g_][1], 0.5), __dmul_rn(tp[g_][2], 0.5));
+          }
+        }
+        if (!LINEAR) {
+          double m0[7], m1[7], m2[7], m3[7];
+#pragma unroll
+          for (int g_ = 0; g_ < 7; g_++)
+            if (g_ < ng) m0[g_] = __dmul_rn(tp[g_][0], W0), m1[g_] = __dmul_rn(tp[g_][1], W1);
+#pragma unroll
+          for (int g_ = 0; g_ < 7; g_++)
+            if (g_ < ng) m2[g_] = __dmul_rn(tp[g_][2], W1), m3[g_] = __dmul_rn(tp[g_][3], W0);
+#pragma unroll
+          for (int g_ = 0; g_ < 7; g_++)
+            if (g_ < ng) res[g_] = __dadd_rn(m0[g_], m1[g_]);
+#pragma unroll
+          for (int g_ = 0; g_ < 7; g_++)
+            if (g_ < ng) res[g_] = __dadd_rn(res[g_], m2[g_]);
+#pragma unroll
+          for (int g_ = 0; g_ < 7; g_++)
+            if (g_ < ng) res[g_] = __dadd_rn(res[g_], m3[g_]);
+        }
+      };
+      constexpr int NB = 5;
+      double p[NB], o[NB], rv[NB];
+      int cd[NB];
+      bool lv[NB], em[NB];
+      auto batch = [&](int n, const int* f_lin, const int* slot) {
+        if (!DEC) {
+          double err[NB], u[NB], f[NB], fr[NB];
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) err[j] = __dsub_rn(o[j], p[j]);
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) u[j] = __dmul_rn(fabs(err[j]), q.inv);
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) u[j] = __dadd_rn(u[j], 0.5);
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) f[j] = floor(u[j]);
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) fr[j] = __dsub_rn(u[j], f[j]);
+          unsigned ex = 0;
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) ex |= (!(fr[j] > 0x1p-40 && fr[j] < 1.0 - 0x1p-40) && !(u[j] >= 200.5)) ? (1u << j) : 0u;
+          if (ex) {
+#pragma unroll
+            for (int j = 0; j < NB; j++)
+              if (j < n && ((ex >> j) & 1)) f[j] = floor(__dadd_rn(__ddiv_rn(fabs(err[j]), q.two_eb), 0.5));
+          }
+          double qv[NB], r[NB], st[NB];
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) qv[j] = copysign(f[j], err[j]);
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) r[j] = __dmul_rn(q.two_eb, qv[j]);
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) r[j] = __dadd_rn(p[j], r[j]);
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) st[j] = sizeof(T) == 4 ? (double)__double2float_rn(r[j]) : r[j];
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) st[j] = __dsub_rn(o[j], st[j]);
+#pragma unroll
+          for (int j = 0; j < NB; j++) {
+            if (j < n) {
+              const bool ok = fabs(qv[j]) <= 127.0 && fabs(st[j]) <= q.eb;
+              rv[j] = ok ? r[j] : o[j];
+              cd[j] = ok ? (int)__dadd_rn(qv[j], 128.0) : 0;
+            }
+          }
+          unsigned rare = 0;
+#pragma unroll
+          for (int j = 0; j < NB; j++) {
+            if (j >= n) break;
+            if (em[j]) A.seq[slot[j]] = (uint8_t)cd[j];
+            const unsigned d = (unsigned)cd[j] - 127u;
+            q.hp += (em[j] && d < 3u) ? (1ull << (21 * d)) : 0ull;
+            rare |= (em[j] && d >= 3u) ? (1u << j) : 0u;
+          }
+          if (rare) {
+#pragma unroll
+            for (int j = 0; j < NB; j++)
+              if (j < n && ((rare >> j) & 1)) {
+                atomicAdd(&shist[cd[j]], 1u);
+                if (cd[j] == 0) {
+                  atomicOr(&A.obm[(unsigned)f_lin[j] >> 5], 1u << (f_lin[j] & 31));
+                  q.bad |= !isfinite(o[j]);
+                }
+              }
+          }
+        } else {
+          double r[NB];
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) r[j] = __dsub_rn((double)cd[j], 128.0);
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) r[j] = __dmul_rn(q.two_eb, r[j]);
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) rv[j] = __dadd_rn(p[j], r[j]);
+          unsigned z = 0;
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+            if (j < n) z |= (lv[j] && cd[j] == 0) ? (1u << j) : 0u;
+          if (z) {
+#pragma unroll
+            for (int j = 0; j < NB; j++)
+              if (j < n && ((z >> j) & 1))
+                rv[j] = m_outlier(A.oidx, A.oval, (unsigned long long)(unsigned)f_lin[j], q.ocount, &q.bad);
+          }
+#pragma unroll
+          for (int j = 0; j < NB; j++) {
+            if (j >= n) break;
+            if (em[j]) {
+              reinterpret_cast<T*>(A.out)[f_lin[j]] = (T)rv[j];
+              q.nf |= !isfinite(rv[j]);
+            }
+          }
+        }
+      };
+      // ---- half 1: c2, c4 of plane k | c1 of odd m1 | c7 of odd m7 | halo of c2 / c4 / c1
+      {
+        const double* e0 = sE + ((m1 - 1) & ME) * G::SE;
+        const double* e1 = sE + (m1 & ME) * G::SE;
+        const double* e2 = sE + ((m1 + 1) & ME) * G::SE;
+        const double* e3 = sE + ((m1 + 2) & ME) * G::SE;
+        const double* s0 = sC6 + ((m7 - 1) & MC) * G::S6;
+        const double* s1 = sC6 + (m7 & MC) * G::S6;
+        const double* s2 = sC6 + ((m7 + 1) & MC) * G::S6;
+        const double* s3 = sC6 + ((m7 + 2) & MC) * G::S6;
+        // halo taps: along x (c1) from the E planes at ea, else in plane k at ea + t * sa
+        const bool hx = hcA == 1;
+        const int sa = hcA == 4 ? 1 : G::EZP, ea = hcA == 4 ? hA.ez : hA.e;
+        double tp[7][4], res[7];
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+          tp[0][t] = Ek[i2.e + t * G::EZP];
+          tp[1][t] = Ek[i4.ez + t];
+          tp[3][t] = sC5[i7.e + t * G::HZ];
+          tp[4][t] = sC3[i7.ez + t];
+        }
+        tp[2][0] = e0[i1.e], tp[2][1] = e1[i1.e], tp[2][2] = e2[i1.e], tp[2][3] = e3[i1.e];
+        tp[5][0] = s0[i7.e], tp[5][1] = s1[i7.e], tp[5][2] = s2[i7.e], tp[5][3] = s3[i7.e];
+        tp[6][0] = hx ? e0[ea] : Ek[ea];
+        tp[6][1] = hx ? e1[ea] : Ek[ea + sa];
+        tp[6][2] = hx ? e2[ea] : Ek[ea + 2 * sa];
+        tp[6][3] = hx ? e3[ea] : Ek[ea + 3 * sa];
+        const T* fa = hx ? f1 : fe;
+        if (!DEC) {
+          o[0] = (double)fe[i2.f], o[1] = (double)fe[i4.f], o[2] = (double)f1[i1.f], o[3] = (double)f7[i7.f];
+          o[4] = (double)fa[hA.f];
+        } else {
+          cd[0] = k2, cd[1] = k4, cd[2] = k1, cd[3] = k7, cd[4] = kA;
+        }
+        stencils(tp, res, 7);
+        p[0] = res[0], p[1] = res[1], p[2] = res[2], p[4] = res[6];
+        p[3] = __ddiv_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, res[5]), res[3]), res[4]), 3.0);  // axes x, y, z
+        lv[0] = le, lv[1] = le, lv[2] = l1, lv[3] = l7, lv[4] = hcA != 0 && (hx ? l1 : le);
+        em[0] = le && oe, em[1] = le && oe, em[2] = l1, em[3] = l7, em[4] = false;
+        const int slot[NB] = {sbE + i2.slot, sbE + i4.slot, sb1 + i1.slot, sb7 + i7.slot, 0};
+        const int lin[NB] = {lbE + i2.lin, lbE + i4.lin, lb1 + i1.lin, lb7 + i7.lin, (hx ? lb1 : lbE) + hA.lin};
+        batch(NB, lin, slot);
+        if (le) c2k[i2.e] = rv[0], c4k[i4.e] = rv[1];
+        if (l1) sC1[i1.e] = rv[2];
+        if (lv[4]) (hx ? sC1 : (hcA == 2 ? c2k : c4k))[hA.e] = rv[4];
+        if (DEC && LV1 && le && oe) {  // the 2-lattice points of plane k are outputs too
+          const double v = Ek[i1.e];
+          reinterpret_cast<T*>(A.out)[lbE + i1.lin] = (T)v;
+          q.nf |= !isfinite(v);
+        }
+      }
+      __syncthreads();
+      // the inputs of phase k+1 land in the slots of planes k-3 (E, odd
+      // field) and k-1 (even field), free from here on
+      stage(k + 1);
+      // ---- half 2: c6 of plane k | c3, c5 of odd m1 | halo of c3 / c5
+      {
+        const double* b0 = sC2 + ((m1 - 1) & MC) * G::S2;
+        const double* b1 = sC2 + (m1 & MC) * G::S2;
+        const double* b2 = sC2 + ((m1 + 1) & MC) * G::S2;
+        const double* b3 = sC2 + ((m1 + 2) & MC) * G::S2;
+        const double* d0 = sC4 + ((m1 - 1) & MC) * G::S4;
+        const double* d1 = sC4 + (m1 & MC) * G::S4;
+        const double* d2 = sC4 + ((m1 + 1) & MC) * G::S4;
+        const double* d3 = sC4 + ((m1 + 2) & MC) * G::S4;
+        const bool h3 = hcB == 3;
+        const double *x0 = h3 ? b0 : d0, *x1 = h3 ? b1 : d1, *x2 = h3 ? b2 : d2, *x3 = h3 ? b3 : d3;
+        const int sb = h3 ? G::EZP : 1, eb = h3 ? hB.e : hB.ez;
+        double tp[7][4], res[7];
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+          tp[0][t] = c4k[i6.e + t * G::HZ];  // c6 along y
+          tp[1][t] = c2k[i6.ez + t];         // c6 along z
+          tp[3][t] = sC1[i3.e + t * G::EZP];  // c3 along y
+          tp[5][t] = sC1[i5.ez + t];          // c5 along z
+          tp[6][t] = sC1[eb + t * sb];        // halo in plane
+        }
+        tp[2][0] = b0[i3.e], tp[2][1] = b1[i3.e], tp[2][2] = b2[i3.e], tp[2][3] = b3[i3.e];  // c3 along x
+        tp[4][0] = d0[i5.e], tp[4][1] = d1[i5.e], tp[4][2] = d2[i5.e], tp[4][3] = d3[i5.e];  // c5 along x
+        double hxv[4] = {x0[hB.e], x1[hB.e], x2[hB.e], x3[hB.e]};
+        if (!DEC) {
+          o[0] = (double)fe[i6.f], o[1] = (double)f1[i3.f], o[2] = (double)f1[i5.f], o[3] = (double)f1[hB.f];
+        } else {
+          cd[0] = k6, cd[1] = k3, cd[2] = k5, cd[3] = kB;
+        }
+        stencils(tp, res, 7);
+        double hres[1];
+        {
+          double htp[1][4] = {{hxv[0], hxv[1], hxv[2], hxv[3]}};
+          stencils(htp, hres, 1);
+        }
+        auto avg2 = [](double a, double b) { return __dmul_rn(__dadd_rn(__dadd_rn(0.0, a), b), 0.5); };
+        p[0] = avg2(res[0], res[1]);  // axes y, z
+        p[1] = avg2(res[2], res[3]);  // x, y
+        p[2] = avg2(res[4], res[5]);  // x, z
+        p[3] = avg2(hres[0], res[6]);  // x, then y (c3) or z (c5)
+        lv[0] = le, lv[1] = l1, lv[2] = l1, lv[3] = hcB != 0 && l1;
+        em[0] = le && oe, em[1] = l1, em[2] = l1, em[3] = false;
+        const int slot[NB] = {sbE + i6.slot, sb1 + i3.slot, sb1 + i5.slot, 0, 0};
+        const int lin[NB] = {lbE + i6.lin, lb1 + i3.lin, lb1 + i5.lin, lb1 + hB.lin, 0};
+        batch(4, lin, slot);
+        if (le) c6k[i6.e] = rv[0];
+        if (l1) sC3[i3.e] = rv[1], sC5[i5.e] = rv[2];
+        if (lv[3]) (h3 ? sC3 : sC5)[hB.e] = rv[3];
+      }
     };
     if (fast)
-      half2(BT<true>{});
+      fast_body();
     else
-      half2(BT<false>{});
+      phase_body(BT<false>{});
     cp_async_wait_all();
     mbar_wait(&bar, phase);
     phase ^= 1;
@@ -663,11 +912,12 @@ bool march_ok(const LevelGeom& g, int cfg) {
 }
 
 int seg_len(const LevelGeom& g) {
-  // enough CTAs for ~3 waves of 148 SMs x 2 resident CTAs, segments of >= 8 even planes
+  // enough CTAs for ~6 waves of 148 SMs x 2 resident CTAs (a short tail),
+  // segments of >= 8 even planes
   const long long tiles = ((g.D[2] + MTZ - 1) / MTZ) * ((g.D[1] + MTY - 1) / MTY);
   const long long nep = (g.D[0] + 1) / 2;
   long long seg = nep;
-  while (seg > 8 && tiles * ((nep + seg - 1) / seg) < 3 * 2 * kSMs) seg = (seg + 1) / 2;
+  while (seg > 8 && tiles * ((nep + seg - 1) / seg) < 6 * 2 * kSMs) seg = (seg + 1) / 2;
   if (const char* e = getenv("HB_MARCH_SEG")) seg = std::max(1, atoi(e));
   return (int)std::max(1ll, seg);
 }
