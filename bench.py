@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--eb", type=float, default=1e-3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config5", action="store_true", help="skip the 2048^3 slab-sharded secondary measurement")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic probe of the dominant kernel")
+    ap.add_argument("--probe", action="store_true", help=argparse.SUPPRESS)  # one compress, for the ncu probe
     return ap.parse_args()
 
 
@@ -187,6 +190,63 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_probe(args):
+    """Child of measure_traffic(): one warm compress, then one compress with
+    the level-1 launches inside a cudaProfilerStart/Stop range (HB_NCU_RANGE)."""
+    import torch
+
+    import paper_2507_11165_b200 as hb
+    from paper_2507_11165_b200 import synth
+    S = args.size
+    f = hb.Field(synth.make_device(args.kind, (S, S, S), seed=2025))
+    spec = hb.ErrorBoundSpec("rel", args.eb)
+    out = torch.empty(hb.compress_bound(f.dims, 4), dtype=torch.uint8, device="cuda")
+    hb.compress_device(f, spec, args.mode, out=out)
+    torch.cuda.synchronize()
+    os.environ["HB_NCU_RANGE"] = "level1"
+    hb.compress_device(f, spec, args.mode, out=out)
+    torch.cuda.synchronize()
+
+
+def measure_traffic(args, timeout=240):
+    """DRAM bytes (read + write) of the level-1 compress kernels, measured in
+    this run: ncu on a child process that compresses the same workload, with
+    only the level-1 launches in the profiled range.  None if ncu is absent."""
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found"
+    cmd = [ncu, "--profile-from-start", "off", "--clock-control", "none", "--csv", "--metrics",
+           "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum", sys.executable,
+           os.path.abspath(__file__), "--probe", "--size", str(args.size), "--kind", args.kind, "--mode", args.mode,
+           "--eb", str(args.eb)]
+    env = dict(os.environ, HB_NCU_RANGE="")
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env)
+    except Exception as e:  # noqa: BLE001
+        return None, f"ncu probe failed: {e}"
+    import csv
+    import io
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    total, kernels, dur = 0.0, set(), 0.0
+    rows = [ln for ln in r.stdout.splitlines() if ln.startswith('"')]
+    for row in csv.DictReader(io.StringIO("\n".join(rows))):
+        m, u, v = row.get("Metric Name"), row.get("Metric Unit"), row.get("Metric Value", "").replace(",", "")
+        try:
+            v = float(v)
+        except ValueError:
+            continue
+        if m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            total += v * scale.get(u, 1)
+            kernels.add(row.get("ID"))
+        elif m == "gpu__time_duration.sum":
+            dur += v * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3,
+                        "ms": 1.0}.get(u, 1e-6)
+    if not kernels:
+        return None, "ncu probe returned no level-1 launches (rc %d): %s" % (r.returncode, r.stderr[-300:])
+    return {"bytes": int(total), "launches": len(kernels), "ncu_ms": round(dur, 4)}, "measured"
+
+
 def cpu_baseline(vals_host, args):
     from oracle import oracle
     cores = os.cpu_count() or 1
@@ -203,9 +263,111 @@ def cpu_baseline(vals_host, args):
         if time.perf_counter() - t0 > 10.0 or reps >= 5:
             break
     dt = time.perf_counter() - t0
+    # one host core: a smaller leading slab, one round trip
+    oracle.set_threads(1)
+    s1 = np.ascontiguousarray(vals_host[:min(vals_host.shape[0], 32)])
+    t1 = time.perf_counter()
+    oracle.decompress(oracle.compress(s1, "rel", args.eb, args.mode, 3))
+    dt1 = time.perf_counter() - t1
+    oracle.set_threads(cores)
     return {"value": round(sample.nbytes * reps / dt / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "port",
             "sample": f"{planes}x{vals_host.shape[1]}x{vals_host.shape[2]} leading slab of the same field, "
-                      f"{reps} round trips, oracle/hb_oracle.c OpenMP"}
+                      f"{reps} round trips, oracle/hb_oracle.c OpenMP",
+            "one_core": {"value": round(s1.nbytes / dt1 / 1e9, 4), "unit": "GB/s", "cores": 1,
+                         "sample": f"{s1.shape[0]}x{s1.shape[1]}x{s1.shape[2]} leading slab, 1 round trip"}}
+
+
+C5_DIMS = (2048, 2048, 2048)
+C5_SLABS = 8
+
+
+def config5(args, world, rank, local, stream):
+    """BASELINE configs[4]: 2048^3 f32 turbulence-like field (32 GiB) as 8
+    axis-0 slabs of 256x2048x2048, split over the N ranks (strong scaling:
+    the volume is fixed, each rank owns 8/N slabs).  Every slab is generated
+    on its own GPU from global coordinates (synth.make_modes); per step:
+    device min/max of the local slabs + one 2-double all-reduce (global
+    rel-eb), compress every local slab, all-gather of the archive sizes
+    (container offsets), decompress every local slab.  No field data crosses
+    GPUs.  Timed like the headline: CUDA events, barrier, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2507_11165_b200 as hb
+    from paper_2507_11165_b200 import _lib, slabs, synth
+    if C5_SLABS % world:
+        return {"unavailable": f"{C5_SLABS} slabs do not split over {world} ranks"}
+    per = C5_SLABS // world
+    bounds = slabs.slab_bounds(C5_DIMS[0], C5_SLABS)[rank * per:(rank + 1) * per]
+    vals = [synth.make_modes((x1 - x0,) + C5_DIMS[1:], seed=2048, x0=x0, global_dims=C5_DIMS) for x0, x1 in bounds]
+    fields = [hb.Field(v) for v in vals]
+    spec = hb.ErrorBoundSpec("rel", args.eb)
+    cap = hb.compress_bound(fields[0].dims, 4)
+    out_buf = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    rec = torch.empty_like(vals[0])
+    grp = dist.group.WORLD if world > 1 else None
+
+    def global_eb():
+        if world > 1:
+            return slabs.global_eb_distributed(fields, spec, np.float32, grp)
+        los, his = zip(*(hb.field.min_max(f) for f in fields))
+        return slabs.global_abs_eb(spec, min(los), max(his), np.float32)
+
+    launches = [0]
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        eb = hb.ErrorBoundSpec("abs", global_eb())
+        launches[0] += _lib.last_launch_count()
+        arcs = []
+        for f in fields:
+            arcs.append(hb.compress_device(f, eb, args.mode, out=out_buf).clone())
+            launches[0] += _lib.last_launch_count()
+        if world > 1:
+            head, offs, total = slabs.container_layout(C5_DIMS, 3, 4, args.mode, bounds, [a.numel() for a in arcs], grp)
+        else:
+            total = slabs.header_bytes(C5_SLABS) + sum(a.numel() for a in arcs)
+        if ev:
+            ev[1].record(stream)
+        for f, a in zip(fields, arcs):
+            hb.decompress_device(a, f.dims, np.float32, out=rec)
+            launches[0] += _lib.last_launch_count()
+        if ev:
+            ev[2].record(stream)
+        return arcs, eb, total
+
+    arcs, eb, total = step()
+    err = (rec.double() - vals[-1].double()).abs().max().item()
+    assert err <= eb.magnitude, (err, eb.magnitude)
+    steps = max(1, min(args.steps, 3))
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    launches[0] = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(steps):
+        arcs, eb, total = step(evs[k])
+    torch.cuda.synchronize()
+    tc = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3
+    td = sum(e[1].elapsed_time(e[2]) for e in evs) / 1e3
+    t = torch.tensor([tc + td, tc, td], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ttot, tcm, tdm = t.tolist()
+    vol = float(np.prod(C5_DIMS)) * 4
+    peak, _ = peaks()
+    res = {"workload": "2048^3 f32 turbulence-like (synth.make_modes), 8 axis-0 slabs of 256x2048x2048, "
+                       f"rel-eb {args.eb} (global), {args.mode.upper()}", "scaling": "strong",
+           "slabs_per_gpu": per, "steps": steps, "warmup": 1,
+           "value": round(vol * steps / ttot / 1e9, 3), "unit": "GB/s",
+           "compress_gbs": round(vol * steps / tcm / 1e9, 3), "decompress_gbs": round(vol * steps / tdm / 1e9, 3),
+           "ms_per_step": round(1e3 * ttot / steps, 3), "cr": round(vol / total, 3), "container_bytes": total,
+           "gpu_launches": launches[0],
+           "hbm_roofline_frac": round(vol * steps / ttot / 1e9 / (peak * world), 5)}
+    del vals, fields, rec, out_buf, arcs
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_ours(args):
@@ -316,15 +478,15 @@ def run_ours(args):
         ms = cand[dom]
         ab = algo_bytes(dom, n, 4, archive_len)
         ach = ab / (ms / 1e3) / 1e9
-        traffic = None
-        try:
-            with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-                traffic = json.load(fh).get(dom)
-        except Exception:
-            pass
+        traffic, tsrc = None, "not measured"
+        if dom == "level1" and rank == 0 and world == 1 and not args.no_traffic:
+            tr, tsrc = measure_traffic(args)
+            if tr:
+                traffic = tr["bytes"]
+                tsrc = f"ncu in this run: {tr['launches']} level-1 launches, {tr['ncu_ms']} ms serialised"
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 2), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic, "algo_bytes": int(ab), "ms": round(ms, 4),
-                "peak_kind": peak_kind,
+                "peak_kind": peak_kind, "traffic_source": tsrc,
                 # DRAM bytes actually moved (ncu, profiles/traffic.json) over the same time: the level
                 # passes trade f64 class round trips through HBM for halo recompute
                 "traffic_gbs": round(traffic / (ms / 1e3) / 1e9, 1) if traffic else None}
@@ -370,6 +532,11 @@ def run_ours(args):
         line["e2e"] = {"value": round(e2e, 3), "unit": "GB/s", "h2d_bytes_per_step": nbytes + len(blob),
                        "d2h_bytes_per_step": len(blob) + nbytes}
 
+    if not args.no_config5:
+        _lib.release_contexts()  # the 512^3 arena is not needed for the slabs
+        torch.cuda.empty_cache()
+        line["config5"] = config5(args, world, rank, local, stream)
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(vals.cpu().numpy(), args)
     if rank == 0:
@@ -380,6 +547,9 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.probe:
+        run_probe(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -95,6 +95,13 @@ HB_API int hb_compress(hb_ctx* ctx, const void* field, int precision, const uint
  * reference subtracts them in the field dtype); FieldError on NaN/Inf. */
 HB_API int hb_value_range(hb_ctx* ctx, const void* field, int precision, uint64_t n, double* vmin, double* vmax);
 
+/* field.py:145-187 quality metrics in one device pass over n values of the
+ * original and the reconstruction (device or host pointers):
+ *   out[0] = sum((o - r)^2) in numpy's pairwise order (mse = out[0] / n, bit-
+ *            identical to np.mean(d * d)),  out[1] = max |o - r|,
+ *   out[2] = min(o), out[3] = max(o)  (value_range subtracts them in dtype). */
+HB_API int hb_quality(hb_ctx* ctx, const void* orig, const void* recon, int precision, uint64_t n, double out[4]);
+
 /* archive.py:93-118 on host bytes (no device work). */
 HB_API int hb_archive_info(const void* host_blob, size_t len, hb_info* info);
 

@@ -59,6 +59,7 @@ def lib():
         L.hb_compress.argtypes = [P, P, I, PU64, I, I, D, I, P, SZ, C.POINTER(SZ), C.POINTER(D), P]
         L.hb_archive_info.argtypes = [P, SZ, C.POINTER(Info)]
         L.hb_value_range.argtypes = [P, P, I, U64, C.POINTER(D), C.POINTER(D)]
+        L.hb_quality.argtypes = [P, P, P, I, U64, C.POINTER(D)]
         L.hb_decompress.argtypes = [P, P, SZ, P, SZ, C.POINTER(Info)]
         L.hb_tune.argtypes = [P, P, I, PU64, D, P, P]
         L.hb_decompose.argtypes = [P, P, I, PU64, D, P, P, P, P, PU64, P]

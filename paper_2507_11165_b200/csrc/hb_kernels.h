@@ -35,6 +35,12 @@ struct LevelGeom {
 
 void make_level_geom(const uint64_t dims[3], int level, LevelGeom* g);
 
+// k_quality.cu: sum of squared differences (numpy pairwise order), max |o - r|,
+// min / max of o -> out_dev[4] (field.py:145-187)
+size_t quality_scratch_bytes(unsigned long long n);
+void launch_quality(const void* orig, const void* recon, int prec, unsigned long long n, void* scratch,
+                    double* out_dev, cudaStream_t s, int* launches);
+
 // field dtype tag
 enum { P32 = 4, P64 = 8 };
 

@@ -21,6 +21,7 @@ between GPUs.
 
 from __future__ import annotations
 
+import os
 import struct
 
 import numpy as np
@@ -120,55 +121,118 @@ def decompress_slabs(blob: bytes, decompress_fn=None) -> Field:
     return Field._trusted(out, ndim)
 
 
-def compress_distributed(local_values, x0: int, global_dims, spec: ErrorBoundSpec, mode: str = "cr",
-                         group=None, compress_fn=None, device=None):
-    """One rank's part of a multi-GPU slab compression.
-
-    local_values: this rank's slab (numpy array or torch tensor), rows
-    [x0, x0 + len) of the global volume.  Collectives (torch.distributed, NCCL
-    on GPUs / gloo on CPU): all-reduce MAX of (max, -min) for the global eb,
-    all-gather of (x0, x1, archive length).  Returns (archive bytes of this
-    slab, byte offset of this archive in the container, container header
-    bytes).  Rank 0 can write the header and every rank its archive at its
-    offset (pwrite / shared buffer) -- see gather_container for a
-    single-writer variant.
-    """
+def _coll_device(group, hint):
+    """Collective buffers: CUDA for NCCL, host for gloo."""
     import torch
     import torch.distributed as dist
-    from . import archive
-    compress_fn = compress_fn or archive.compress
-    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        return hint if hint is not None and torch.device(hint).type == "cuda" else torch.device("cuda")
+    return torch.device("cpu")
+
+
+def global_eb_distributed(local_fields, spec: ErrorBoundSpec, dtype, group=None, device=None) -> float:
+    """Volume-global abs eb from this rank's slabs: device min/max per slab
+    (k_minmax), one all-reduce MAX of (max, -min) -- 2 doubles."""
+    import torch
+    import torch.distributed as dist
     from .field import min_max
-    is_t = isinstance(local_values, torch.Tensor)
-    dev = device or (local_values.device if is_t else torch.device("cpu"))
-    ndim0 = 2 if len(tuple(global_dims)) == 2 else 3
-    lo, hi = min_max(Field(local_values, ndim=ndim0))
-    vmin, vmax = float(lo), float(hi)
-    np_dtype = np.dtype(np.float32) if (local_values.dtype in (np.float32, torch.float32)) else np.dtype(np.float64)
-    mm = torch.tensor([vmax, -vmin], dtype=torch.float64, device=dev)
+    if spec.mode == "abs":
+        return float(spec.magnitude)
+    vmax, nmin = -np.inf, -np.inf
+    for f in local_fields:
+        lo, hi = min_max(f)
+        vmax, nmin = max(vmax, float(hi)), max(nmin, -float(lo))
+    mm = torch.tensor([vmax, nmin], dtype=torch.float64, device=_coll_device(group, device))
     dist.all_reduce(mm, op=dist.ReduceOp.MAX, group=group)
-    gmax, gmin = mm[0].item(), -mm[1].item()
-    eb = global_abs_eb(spec, np_dtype.type(gmin), np_dtype.type(gmax), np_dtype)
-    ndim = 2 if len(tuple(global_dims)) == 2 else 3
-    f = Field(local_values, ndim=ndim)
-    arc = compress_fn(f, ErrorBoundSpec("abs", eb), mode)
-    mine = torch.tensor([x0, x0 + f.dims[0], len(arc)], dtype=torch.int64, device=dev)
+    dt = np.dtype(dtype)
+    return global_abs_eb(spec, dt.type(-mm[1].item()), dt.type(mm[0].item()), dt)
+
+
+def container_layout(global_dims, ndim: int, precision: int, mode: str, local_ranges, local_sizes, group=None,
+                     device=None):
+    """All-gather of every slab's (x0, x1, archive length) -- the only exchange
+    the container needs -- then the prefix offsets.  Returns (header bytes,
+    byte offset of each local archive in the container, total length)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    cdev = _coll_device(group, device)
+    k = len(local_ranges)
+    counts = torch.tensor([k], dtype=torch.int64, device=cdev)
+    allc = [torch.empty_like(counts) for _ in range(world)]
+    dist.all_gather(allc, counts, group=group)
+    kmax = max(int(c.item()) for c in allc)
+    mine = torch.full((kmax, 3), -1, dtype=torch.int64, device=cdev)
+    for i, ((x0, x1), n) in enumerate(zip(local_ranges, local_sizes)):
+        mine[i] = torch.tensor([x0, x1, n], dtype=torch.int64)
     allv = [torch.empty_like(mine) for _ in range(world)]
     dist.all_gather(allv, mine, group=group)
-    table = sorted(tuple(int(x) for x in t.tolist()) for t in allv)
-    bounds = [(a, b) for a, b, _ in table]
-    sizes = [n for _, _, n in table]
+    table = sorted(tuple(int(x) for x in row) for t in allv for row in t.tolist() if row[0] >= 0)
     dims = tuple(int(d) for d in global_dims)
     if len(dims) == 2:
         dims = dims + (1,)
-    hb = header_bytes(world)
-    offs, o = [], hb
-    for n in sizes:
-        offs.append(o)
+    hb = header_bytes(len(table))
+    offs, o = {}, hb
+    for a, b, n in table:
+        offs[a] = o
         o += n
-    my = [i for i, (a, b) in enumerate(bounds) if a == x0][0]
-    head = assemble(dims, ndim, np_dtype.itemsize, mode, bounds, [b"\0" * n for n in sizes])[:hb]
-    return arc, offs[my], head
+    head = _HEAD.pack(MAGIC, VERSION, ndim, precision, _MODES[mode], 0, len(table), *dims)
+    head += b"".join(_ENTRY.pack(a, b, offs[a], n) for a, b, n in table)
+    return head, [offs[x0] for x0, _ in local_ranges], o
+
+
+def compress_distributed_many(local_slabs, global_dims, spec: ErrorBoundSpec, mode: str = "cr", group=None,
+                              compress_fn=None, device=None):
+    """This rank's slabs [(values, x0), ...] of a multi-GPU slab compression:
+    global eb (2-double all-reduce), one archive per slab (no field data
+    crosses GPUs), size all-gather.  Returns (archives, offsets, header)."""
+    from . import archive
+    compress_fn = compress_fn or archive.compress
+    ndim = 2 if len(tuple(global_dims)) == 2 else 3
+    fields = [Field(v, ndim=ndim) for v, _ in local_slabs]
+    dt = fields[0].dtype if fields else np.dtype(np.float32)
+    eb = global_eb_distributed(fields, spec, dt, group, device)
+    arcs = [compress_fn(f, ErrorBoundSpec("abs", eb), mode) for f in fields]
+    ranges = [(x0, x0 + f.dims[0]) for (_, x0), f in zip(local_slabs, fields)]
+    head, offs, _ = container_layout(global_dims, ndim, dt.itemsize, mode, ranges, [len(a) for a in arcs], group,
+                                     device)
+    return arcs, offs, head
+
+
+def compress_distributed(local_values, x0: int, global_dims, spec: ErrorBoundSpec, mode: str = "cr",
+                         group=None, compress_fn=None, device=None):
+    """One slab per rank: (archive of this slab, its byte offset in the
+    container, container header).  See compress_distributed_many."""
+    arcs, offs, head = compress_distributed_many([(local_values, x0)], global_dims, spec, mode, group, compress_fn,
+                                                 device)
+    return arcs[0], offs[0], head
+
+
+def _host_bytes(arc) -> bytes:
+    if isinstance(arc, (bytes, bytearray, memoryview)):
+        return bytes(arc)
+    return arc.cpu().numpy().tobytes()  # device archive (compress_device)
+
+
+def write_container(path: str, head: bytes, archives, offsets, group=None):
+    """Offset writes: every rank pwrites its own archives at their prefix
+    offsets into one shared file; rank 0 writes the header.  No archive bytes
+    cross ranks (the size all-gather already fixed every offset)."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    if rank == 0:
+        with open(path, "wb"):
+            pass
+    dist.barrier(group=group)
+    fd = os.open(path, os.O_WRONLY)
+    try:
+        if rank == 0:
+            os.pwrite(fd, bytes(head), 0)
+        for a, o in zip(archives, offsets):
+            os.pwrite(fd, _host_bytes(a), o)
+    finally:
+        os.close(fd)
+    dist.barrier(group=group)
 
 
 def gather_container(arc: bytes, x0: int, head: bytes, group=None, dst: int = 0):

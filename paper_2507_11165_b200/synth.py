@@ -7,6 +7,10 @@ Not part of the compress/decompress path.  Kinds:
   rough  white noise filtered by 1/(1 + k^2/0.005), normalised to [0, 1]
          (rough, outlier-producing stress case).
   gauss  sum of six random anisotropic Gaussians (very smooth).
+  modes  random-phase spectral synthesis (turbulence-like): a sum
+         of separable Fourier modes with a k^(-11/6) exp(-(k/0.08)^2) amplitude,
+         defined per GLOBAL coordinate, so any axis-0 slab of a huge volume
+         (config 5: 2048^3) is generated on its own GPU without the rest.
 `make` builds host numpy arrays, `make_device` builds torch CUDA tensors with
 the same recipe (values differ between the two; each is deterministic).
 """
@@ -103,3 +107,60 @@ def make_device(kind: str, dims, seed: int = 0, dtype="f32", device="cuda"):
     else:
         raise ValueError(kind)
     return v.to(torch.float32 if dtype in ("f32", np.float32) else torch.float64).contiguous()
+
+
+def _mode_tables(global_dims, seed: int, n_modes: int):
+    """Per-mode wave numbers, phases and amplitudes (host, tiny; numpy RNG)."""
+    d = np.array(_dims3(global_dims), np.float64)
+    rng = np.random.default_rng(seed)
+    # integer wave numbers (periodic over the global box), |k| log-uniform
+    # between the box scale and the 0.08 cycles/point cutoff
+    kmag = np.exp(rng.uniform(np.log(1.0 / d.max()), np.log(0.12), n_modes))
+    u = rng.standard_normal((n_modes, 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    k = np.round(np.abs(u) * kmag[:, None] * d) / d  # cycles per point along each axis
+    k = np.where(d[None, :] > 1, k, 0.0)
+    kk = np.sqrt((k * k).sum(1))
+    amp = np.where(kk > 0, np.maximum(kk, 1e-12) ** (-11.0 / 6.0), 0.0) * np.exp(-(kk / 0.08) ** 2)
+    # density of the log-uniform |k| draw is 1/k: weight by k^(3/2) so the
+    # sum approximates an isotropic k^-11/6 spectrum in 3D
+    amp *= kk ** 1.5
+    amp /= np.sqrt((amp * amp).sum()) + 1e-300
+    phase = rng.uniform(0, 2 * np.pi, (n_modes, 3))
+    return k, phase, amp
+
+
+def make_modes(dims, seed: int = 0, dtype="f32", x0: int = 0, global_dims=None, n_modes: int = 96,
+               device="cuda"):
+    """Rows [x0, x0 + dims[0]) of the global `modes` field, on the GPU.
+
+    v(x, y, z) = sum_m a_m cos(2 pi kx_m x + px_m) cos(2 pi ky_m y + py_m) cos(2 pi kz_m z + pz_m)
+    evaluated as one (ny, M) x (M, nz) GEMM per x-plane (fp32 or fp64 cuBLAS,
+    TF32 off), so the value at a global coordinate never depends on the slab
+    that contains it."""
+    import torch
+    d = _dims3(dims)
+    gd = _dims3(global_dims) if global_dims is not None else d
+    k, ph, amp = _mode_tables(gd, seed, n_modes)
+    tdt = torch.float32 if dtype in ("f32", np.float32) else torch.float64
+
+    def axis(a, lo, n):
+        c = torch.arange(lo, lo + n, dtype=torch.float64, device=device)
+        kt = torch.tensor(k[:, a], dtype=torch.float64, device=device)
+        pt = torch.tensor(ph[:, a], dtype=torch.float64, device=device)
+        return torch.cos(2 * np.pi * kt[:, None] * c[None, :] + pt[:, None])  # (M, n)
+
+    A = axis(0, x0, d[0]) * torch.tensor(amp, dtype=torch.float64, device=device)[:, None]
+    B = axis(1, 0, d[1]).to(tdt)
+    C = axis(2, 0, d[2]).to(tdt)
+    A = A.to(tdt)
+    out = torch.empty(d, dtype=tdt, device=device)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        Bt = B.t().contiguous()
+        for i in range(d[0]):  # one GEMM shape for every plane of every slab
+            torch.mm(Bt * A[:, i][None, :], C, out=out[i])
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return out

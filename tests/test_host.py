@@ -135,3 +135,32 @@ def test_gpu_path_fails_loudly_without_cuda():
         pytest.skip("has a GPU")
     with pytest.raises(RuntimeError):
         hb.compress(hb.Field(np.zeros((4, 4, 4), np.float32)), hb.ErrorBoundSpec("abs", 1e-3))
+
+
+def test_cli_parser_mirrors_reference():
+    """Sub-commands, flags and run-record columns of reference cli.py:236-333."""
+    from paper_2507_11165_b200 import cli
+    p = cli.build_parser()
+    a = p.parse_args(["compress", "-i", "x", "-t", "f32", "-d", "4", "5", "6", "-m", "rel", "-e", "1e-3", "-o", "y"])
+    assert (a.command, a.mode, tuple(a.dims), a.error_mode, a.error_bound) == ("compress", "cr", (4, 5, 6), "rel",
+                                                                               1e-3)
+    a = p.parse_args(["sweep", "-i", "x", "--dataset", "cesm-atm", "-m", "rel", "-e", "1e-2", "1e-3", "--csv", "o"])
+    assert a.modes == ["cr", "tp"] and a.error_bounds == [1e-2, 1e-3]
+    assert set(cli.COMMANDS) == {"compress", "decompress", "analyze", "sweep", "gen"}
+    assert len(cli.RUN_RECORD_COLUMNS) == 24 and cli.RUN_RECORD_COLUMNS[14] == "psnr_db"
+    with pytest.raises(SystemExit) as e:
+        cli.main(["compress", "-i", "x", "-m", "rel", "-e", "1", "-o", "y"])  # no -t / -d
+    assert e.value.code == 2
+    svg = cli.rd_svg({"cr": [(1.0, 40.0), (2.0, 60.0)], "tp": [(1.5, float("inf"))]})
+    assert svg.startswith("<svg") and svg.count("<polyline") == 1
+
+
+def test_modes_generator_is_per_global_coordinate():
+    """synth.make_modes: any axis-0 slab equals the same rows of the whole
+    volume (config-5 slabs are generated independently per GPU)."""
+    import torch
+    from paper_2507_11165_b200 import synth
+    full = synth.make_modes((24, 20, 18), seed=5, device="cpu")
+    parts = [synth.make_modes((b - a, 20, 18), seed=5, x0=a, global_dims=(24, 20, 18), device="cpu")
+             for a, b in ((0, 7), (7, 16), (16, 24))]
+    assert torch.equal(torch.cat(parts), full)

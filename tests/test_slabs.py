@@ -108,3 +108,93 @@ def test_gpu_slab_container_matches_oracle(oracle):
     assert gpu == ref
     out = slabs.decompress_slabs(gpu)
     assert np.max(np.abs(out.values.astype(np.float64) - vals)) <= oracle.resolve_eb(vals, "rel", 1e-3)
+
+
+def _worker_many(rank, world, port, vals, q, path, use_gpu):
+    """Two slabs per rank (the config-5 layout at small size): global eb
+    all-reduce, size all-gather, offset writes into one shared file."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    bounds = slabs.slab_bounds(vals.shape[0], 2 * world)[2 * rank:2 * rank + 2]
+    spec = hb.ErrorBoundSpec("rel", 1e-3)
+    if use_gpu:
+        import torch
+        local = [(torch.from_numpy(np.ascontiguousarray(vals[a:b])).cuda(), a) for a, b in bounds]
+        fn = hb.compress_device
+    else:
+        local = [(np.ascontiguousarray(vals[a:b]), a) for a, b in bounds]
+        fn = oracle_compress
+    arcs, offs, head = slabs.compress_distributed_many(local, vals.shape, spec, "cr", compress_fn=fn)
+    slabs.write_container(path, head, arcs, offs)
+    q.put((rank, offs, [len(a) for a in arcs]))
+    dist.destroy_process_group()
+
+
+def _run_many(vals, path, use_gpu):
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_many, args=(r, 2, port, vals, q, path, use_gpu)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    return res
+
+
+def test_distributed_offset_writes_gloo_world2(oracle, tmp_path):
+    vals = synth.make("grf", (44, 30, 26), seed=6)
+    path = str(tmp_path / "c.cszs")
+    _run_many(vals, path, use_gpu=False)
+    blob = open(path, "rb").read()
+    single = slabs.compress_slabs(hb.Field(vals), hb.ErrorBoundSpec("rel", 1e-3), "cr", 4,
+                                  compress_fn=oracle_compress)
+    assert blob == single  # offset-written file == single-process container
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_gpu_distributed_world2_matches_oracle(oracle, tmp_path):
+    """Two ranks (gloo; one GPU shared) drive the CUDA compressor on CUDA
+    tensors; the offset-written container equals the oracle's, slab by slab."""
+    vals = synth.make_modes((64, 96, 80), seed=4, device="cuda").cpu().numpy()
+    path = str(tmp_path / "g.cszs")
+    _run_many(vals, path, use_gpu=True)
+    blob = open(path, "rb").read()
+    ref = slabs.compress_slabs(hb.Field(vals), hb.ErrorBoundSpec("rel", 1e-3), "cr", 4, compress_fn=oracle_compress)
+    assert blob == ref
+    out = slabs.decompress_slabs(blob)
+    assert np.max(np.abs(out.values.astype(np.float64) - vals)) <= oracle.resolve_eb(vals, "rel", 1e-3)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_gpu_config5_slab_matches_oracle(oracle):
+    """One full config-5 slab (rows 768..1024 of the 2048^3 field, generated
+    on the GPU from global coordinates) byte-identical to the oracle under the
+    volume-global eb -- the per-slab parity behind bench.py's config5 line."""
+    import torch
+    oracle.set_threads(0)
+    g = (2048, 2048, 2048)
+    v = synth.make_modes((256, 2048, 2048), seed=2048, x0=768, global_dims=g)
+    # global eb from all 8 slabs' min/max (as the bench computes it)
+    lo, hi = np.inf, -np.inf
+    for x0 in range(0, 2048, 256):
+        s = v if x0 == 768 else synth.make_modes((256, 2048, 2048), seed=2048, x0=x0, global_dims=g)
+        lo, hi = min(lo, float(s.min())), max(hi, float(s.max()))
+        del s
+    eb = slabs.global_abs_eb(hb.ErrorBoundSpec("rel", 1e-3), np.float32(lo), np.float32(hi), np.float32)
+    f = hb.Field(v)
+    arch = hb.compress_device(f, hb.ErrorBoundSpec("abs", eb), "cr")
+    host = v.cpu().numpy()
+    ref = oracle.compress(host, "abs", eb, "cr", 3)
+    assert arch.cpu().numpy().tobytes() == ref
+    back, _ = oracle.decompress(ref)
+    out = hb.decompress_device(arch, f.dims, np.float32)
+    assert np.array_equal(out.values.cpu().numpy().reshape(-1), back.reshape(-1))
+    del v, f, arch, out
+    torch.cuda.empty_cache()
