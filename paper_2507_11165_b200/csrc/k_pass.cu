@@ -246,31 +246,43 @@ __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, 
 // One CTA's tile of class k.  CLSC >= 0: that class is known at compile time
 // and interpolates along all its odd axes (multidim) -- every parity test,
 // tap stride and slot term folds; CLSC < 0: class and axes from the arguments
-template <typename T, bool DEC, int K, bool LINEAR, bool LV1, int CLSC, int TX>
-__device__ __forceinline__ void tp_block(const TPassArgs& A, const TMaps& M, int k, int bx, double* tiles,
-                                         unsigned* shist, uint64_t& bar) {
+// SWEEP: called from the persistent level-1 sweep (k_tsweep) -- the block
+// coordinates come from the work item, the mbarrier was initialised once and
+// completes phase `phase`, the histogram is flushed once per CTA at the end.
+// Returns whether the block had work (and so used a barrier phase).
+template <typename T, bool DEC, int K, bool LINEAR, bool LV1, int CLSC, int TX, bool SWEEP = false>
+__device__ __forceinline__ bool tp_block(const TPassArgs& A, const TMaps& M, int k, int bx, double* tiles,
+                                         unsigned* shist, uint64_t& bar, int by = -1, int bz = -1,
+                                         unsigned phase = 0) {
   const LevelGeom& g = A.g;
   const int CLS = CLSC >= 0 ? CLSC : A.cls[k], AXM = CLSC >= 0 ? CLSC : A.axm[k];
   const int n0 = cdim1(g, CLS, 0), n1 = cdim1(g, CLS, 1), n2 = cdim1(g, CLS, 2);
-  const int x0 = bx * TX, y0 = blockIdx.y * TY, z0 = blockIdx.x * TZ;
-  if (x0 >= n0 || y0 >= n1 || z0 >= n2) return;  // block past this class's extent (uniform)
+  const int x0 = bx * TX, y0 = (SWEEP ? by : (int)blockIdx.y) * TY, z0 = (SWEEP ? bz : (int)blockIdx.x) * TZ;
+  if (x0 >= n0 || y0 >= n1 || z0 >= n2) return false;  // block past this class's extent (uniform)
   const int yl = threadIdx.x >> 5, zl = threadIdx.x & 31;
   const int y = y0 + yl, z = z0 + zl;
   const int nx = min(TX, n0 - x0);
   __shared__ double s_eb[3];
   __shared__ unsigned long long s_ocount;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (!SWEEP) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      s_eb[0] = A.st->eb;
+      s_eb[1] = A.st->two_eb;
+      s_eb[2] = __ddiv_rn(1.0, s_eb[1]);  // one IEEE division per block
+      s_ocount = DEC ? *A.ocount : 0;
+    }
+    if (!DEC)
+      for (int i = threadIdx.x; i < 256; i += T_THREADS) shist[i] = 0;
+    __syncthreads();
+  } else if (threadIdx.x == 0) {
     s_eb[0] = A.st->eb;
     s_eb[1] = A.st->two_eb;
-    s_eb[2] = __ddiv_rn(1.0, s_eb[1]);  // one IEEE division per block
+    s_eb[2] = __ddiv_rn(1.0, s_eb[1]);
     s_ocount = DEC ? *A.ocount : 0;
   }
-  if (!DEC)
-    for (int i = threadIdx.x; i < 256; i += T_THREADS) shist[i] = 0;
-  __syncthreads();
   if (threadIdx.x == 0) {
     unsigned bytes = 0;
     int m = AXM;
@@ -330,10 +342,11 @@ __device__ __forceinline__ void tp_block(const TPassArgs& A, const TMaps& M, int
         full &= LINEAR ? (Phi + 1 < g.D[a]) : (Plo >= 3 && Phi + 3 < g.D[a]);
       }
   }
+  if (SWEEP) __syncthreads();  // s_eb / s_ocount
   const double eb = s_eb[0], two_eb = s_eb[1], inv_two_eb = s_eb[2];
   const unsigned long long ocount = s_ocount;
   Acc acc{0u, 0u, 0u, false, false};
-  mbar_wait(&bar, 0);
+  mbar_wait(&bar, phase);
   if (live) {
     if (full)
       tp_run<T, DEC, K, LINEAR, true, LV1, TX>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb, two_eb, inv_two_eb, ocount,
@@ -352,10 +365,13 @@ __device__ __forceinline__ void tp_block(const TPassArgs& A, const TMaps& M, int
       if (h8) atomicAdd(&shist[128], h8);
       if (h9) atomicAdd(&shist[129], h9);
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < 256; i += T_THREADS)
-      if (shist[i]) atomicAdd(&A.st->hist[i], (unsigned long long)shist[i]);
+    if (!SWEEP) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < 256; i += T_THREADS)
+        if (shist[i]) atomicAdd(&A.st->hist[i], (unsigned long long)shist[i]);
+    }
   }
+  return true;
 }
 
 // A dependency step.  C0..C2 >= 0: the step's classes (multidim, all odd
@@ -383,6 +399,126 @@ __global__ void __launch_bounds__(T_THREADS, C0 >= 0 ? 4 : 2) k_tpass(const __gr
         tp_block<T, DEC, K, LINEAR, LV1, C2, TX>(A, M, k, bx, tiles, shist, bar);
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Level 1 (multidim) as ONE persistent sweep along axis 0.
+//
+// The seven per-class passes above each stream the whole volume, so the f64
+// class arrays one step writes are evicted before the next step reads them,
+// and the E lattice and both z-parities of every field sector are fetched by
+// several launches (4.9x the algorithmic DRAM bytes at 512^3).  Here the
+// class lattice is cut into x-slabs of SX planes and the work items (one
+// 4 x 8 x 32 block of one class) are handed out by an atomic ticket in stage
+// order
+//     stage t:  step 1 (classes 1, 2, 4) of slab t,
+//               step 2 (classes 3, 5, 6) of slab t - 2,
+//               step 3 (class 7)         of slab t - 4,
+// so a step reads what the previous step wrote about one stage earlier (a
+// few MB per slab: still in L2) and the field rows shared by two classes of a
+// slab are read from HBM once.  A step-q item of slab j waits (one thread,
+// acquire loads) until step q-1 has finished slabs j-1..j+1 -- its stencils
+// reach +-3 lattice points = +-2 class planes, never past the neighbour slab
+// (SX >= 2).  Tickets are taken in list order by resident CTAs and every
+// dependency points to a smaller ticket, so the sweep cannot deadlock for any
+// grid size.  The bodies are the class-specialised blocks of k_tpass
+// (tp_block), bit for bit the same arithmetic.
+constexpr int SX = 4;     // class planes per slab
+constexpr int SKEW = 2;   // stages between dependent steps
+
+struct SweepArgs {
+  TPassArgs A[3];  // step q: classes / maps of the step (plan_step)
+  int nslab, nby, nbz, nitems;
+  int I[3];        // items per slab of step q
+  unsigned* ticket;
+  unsigned* done;  // [3][nslab] finished items per (step, slab)
+};
+struct alignas(64) SweepMaps {
+  TMaps M[3];
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__host__ __device__ __forceinline__ int stage_items(const SweepArgs& S, int t) {
+  return (t < S.nslab ? S.I[0] : 0) + (t >= SKEW && t - SKEW < S.nslab ? S.I[1] : 0) +
+         (t >= 2 * SKEW && t - 2 * SKEW < S.nslab ? S.I[2] : 0);
+}
+
+template <typename T, bool DEC, bool LINEAR>
+__global__ void __launch_bounds__(T_THREADS, 3) k_tsweep(const __grid_constant__ SweepArgs S,
+                                                        const __grid_constant__ SweepMaps SM) {
+  extern __shared__ __align__(128) double tiles[];
+  __shared__ unsigned shist[256];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int s_it;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (!DEC)
+    for (int i = threadIdx.x; i < 256; i += T_THREADS) shist[i] = 0;
+  unsigned ph = 0;
+  int t = 0, tstart = 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_it = (int)atomicAdd(S.ticket, 1u);
+    __syncthreads();
+    const int it = s_it;
+    if (it >= S.nitems) break;
+    while (it >= tstart + stage_items(S, t)) tstart += stage_items(S, t++);
+    int l = it - tstart, q = 0, j = t;
+    if (t < S.nslab && l < S.I[0]) {
+      q = 0, j = t;
+    } else {
+      if (t < S.nslab) l -= S.I[0];
+      if (t >= SKEW && t - SKEW < S.nslab && l < S.I[1]) {
+        q = 1, j = t - SKEW;
+      } else {
+        if (t >= SKEW && t - SKEW < S.nslab) l -= S.I[1];
+        q = 2, j = t - 2 * SKEW;
+      }
+    }
+    if (q > 0 && threadIdx.x == 0) {
+      const unsigned* d = S.done + (q - 1) * S.nslab;
+      const unsigned need = (unsigned)S.I[q - 1];
+      for (int jj = max(0, j - 1); jj <= min(S.nslab - 1, j + 1); jj++)
+        while (ld_acquire(d + jj) < need) __nanosleep(32);
+      // the class arrays written by those items are read through the async (TMA) proxy
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    const int ncls = q == 1 ? 3 : (q == 0 ? 3 : 1);
+    const int k = l % ncls;
+    const int r = l / ncls;
+    const int zb = r % S.nbz, yb = (r / S.nbz) % S.nby, xb = r / (S.nbz * S.nby);
+    const int bx = j * (SX / 4) + xb;
+    bool used;
+    if (q == 0) {
+      used = k == 0   ? tp_block<T, DEC, 1, LINEAR, true, 1, 4, true>(S.A[0], SM.M[0], 0, bx, tiles, shist, bar, yb, zb, ph & 1)
+             : k == 1 ? tp_block<T, DEC, 1, LINEAR, true, 2, 4, true>(S.A[0], SM.M[0], 1, bx, tiles, shist, bar, yb, zb, ph & 1)
+                      : tp_block<T, DEC, 1, LINEAR, true, 4, 4, true>(S.A[0], SM.M[0], 2, bx, tiles, shist, bar, yb, zb, ph & 1);
+    } else if (q == 1) {
+      used = k == 0   ? tp_block<T, DEC, 2, LINEAR, true, 3, 4, true>(S.A[1], SM.M[1], 0, bx, tiles, shist, bar, yb, zb, ph & 1)
+             : k == 1 ? tp_block<T, DEC, 2, LINEAR, true, 5, 4, true>(S.A[1], SM.M[1], 1, bx, tiles, shist, bar, yb, zb, ph & 1)
+                      : tp_block<T, DEC, 2, LINEAR, true, 6, 4, true>(S.A[1], SM.M[1], 2, bx, tiles, shist, bar, yb, zb, ph & 1);
+    } else {
+      used = tp_block<T, DEC, 3, LINEAR, true, 7, 4, true>(S.A[2], SM.M[2], 0, bx, tiles, shist, bar, yb, zb, ph & 1);
+    }
+    ph += used ? 1u : 0u;
+    __syncthreads();  // tiles free for the next item; this item's stores issued
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(S.done + q * S.nslab + j, 1u);
+    }
+  }
+  if (!DEC) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += T_THREADS)
+      if (shist[i]) atomicAdd(&S.A[0].st->hist[i], (unsigned long long)shist[i]);
   }
 }
 
@@ -508,13 +644,13 @@ int map_for(Launch& L, int cn, int a, int tx, int keys[6]) {
 }
 
 // builds the maps of one dependency step (false = not expressible as TMA boxes)
-bool plan_step(Launch& L, int K, const int* cls, const int* axm, int n) {
+bool plan_step(Launch& L, int K, const int* cls, const int* axm, int n, int tx_override = 0) {
   TPassArgs& A = L.A;
   A.ncls = n;
   L.nmaps = 0;
   int keys[6] = {-1, -1, -1, -1, -1, -1};
   long long mx = 0;
-  const int tx = txof(K);
+  const int tx = tx_override ? tx_override : txof(K);
   for (int k = 0; k < n; k++) {
     A.cls[k] = cls[k];
     A.axm[k] = axm[k];
@@ -557,6 +693,60 @@ void launch_step(const Launch& L, cudaStream_t s, int* launches) {
   (*launches)++;
 }
 
+long long class_stride(const LevelGeom& g);
+
+// counters of the level-1 sweep live after the seven class arrays
+unsigned* sweep_counters(const Launch& L) {
+  return reinterpret_cast<unsigned*>(L.A.scr + 7 * L.A.cstride);
+}
+int sweep_slabs(const LevelGeom& g) { return (int)(((g.D[0] + 1) / 2 + SX - 1) / SX); }
+
+bool sweep_on() {
+  static const int v = [] {
+    const char* e = getenv("HB_SWEEP");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
+template <typename T, bool DEC, bool LINEAR>
+bool launch_sweep(const Launch& base, cudaStream_t s, int* launches) {
+  Launch L[3] = {base, base, base};
+  const int c1[3] = {1, 2, 4}, c2[3] = {3, 5, 6}, c3[1] = {7};
+  if (!plan_step(L[0], 1, c1, c1, 3, 4) || !plan_step(L[1], 2, c2, c2, 3, 4) || !plan_step(L[2], 3, c3, c3, 1, 4))
+    return false;
+  static_assert(SX % 4 == 0 && SX / 4 >= 1, "slab = whole 4-plane blocks");
+  SweepArgs S;
+  SweepMaps SM;
+  for (int q = 0; q < 3; q++) {
+    S.A[q] = L[q].A;
+    SM.M[q] = L[q].M;
+  }
+  const LevelGeom& g = base.A.g;
+  S.nslab = sweep_slabs(g);
+  S.nby = (int)((((g.D[1] + 1) / 2) + TY - 1) / TY);
+  S.nbz = (int)((((g.D[2] + 1) / 2) + TZ - 1) / TZ);
+  S.I[0] = 3 * (SX / 4) * S.nby * S.nbz;
+  S.I[1] = 3 * (SX / 4) * S.nby * S.nbz;
+  S.I[2] = (SX / 4) * S.nby * S.nbz;
+  S.nitems = S.nslab * (S.I[0] + S.I[1] + S.I[2]);
+  S.ticket = sweep_counters(base);
+  S.done = S.ticket + 1;
+  cudaMemsetAsync(S.ticket, 0, sizeof(unsigned) * (1 + 3 * (size_t)S.nslab), s);
+  const size_t smem = (size_t)3 * slot_of(4) * 8;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute((const void*)k_tsweep<T, DEC, LINEAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tsweep<T, DEC, LINEAR>, T_THREADS, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int grid = std::min(S.nitems, kSMs * per_sm);
+  k_tsweep<T, DEC, LINEAR><<<grid, T_THREADS, smem, s>>>(S, SM);
+  (*launches) += 2;
+  return true;
+}
+
 // the three dependency steps of level 1; every map is built before anything
 // is launched, so a shape TMA cannot express falls back cleanly
 template <typename T, bool DEC, bool LINEAR, bool LV1>
@@ -572,6 +762,7 @@ bool run_passes(const Launch& base, int cfg, cudaStream_t s, int* launches) {
     launch_step<T, DEC, 3, LINEAR, LV1>(L[2], s, launches);
     return true;
   }
+  if ((cfg & 2) == 0 && LV1 && sweep_on() && launch_sweep<T, DEC, LINEAR>(base, s, launches)) return true;
   if ((cfg & 2) == 0 && !DEC) {  // multidim, level-1 compress: one launch per specialised class
     // (measured faster than the grouped launch below for the quantizing
     // kernels: a single class body keeps the instruction footprint small)
@@ -649,7 +840,7 @@ size_t level_scratch_bytes(const uint64_t dims[3]) {
   // L >= 2 needs seven arrays of 1/8^(L-1) the size
   LevelGeom g;
   make_level_geom(dims, 1, &g);
-  return (size_t)7 * class_stride(g) * 8 + 256;
+  return (size_t)7 * class_stride(g) * 8 + sizeof(unsigned) * (4 + 3 * (size_t)sweep_slabs(g)) + 256;
 }
 
 int launch_level_pass_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq, uint32_t* obm,
