@@ -243,9 +243,153 @@ __device__ __forceinline__ void tp_run(const TPassArgs& A, const double* tiles, 
   }
 }
 
+// ---- level 1, multidim, class known at compile time: the hot loop.
+// Everything per target that does not depend on the target is hoisted: the
+// interpolation axes and their shared-memory tap strides are compile-time
+// constants, the originals / codes are in registers, the code byte, the f64
+// reconstruction and the output are written through per-thread pointers
+// stepped by runtime strides, the rare paths (exact-division fallback of the
+// quantizer, outliers, orphan codes) are out of line, and the 127/128/129
+// histogram bins are counted branch-free in registers.
+
+// floor(|err| / two_eb + 0.5) by IEEE division (quantize_fast's fallback)
+__device__ __noinline__ double q_exact(double ae, double two_eb) {
+  return floor(__dadd_rn(__ddiv_rn(ae, two_eb), 0.5));
+}
+
+__device__ __noinline__ void note_outlier(uint32_t* obm, unsigned long long li) {
+  atomicOr(&obm[li >> 5], 1u << (li & 31));
+}
+
+template <bool CAST32>
+__device__ __forceinline__ int quantize_lv1(double o, double p, double eb, double two_eb, double inv_two_eb,
+                                            double* recon) {
+  const double err = __dsub_rn(o, p);
+  const double ae = fabs(err);
+  const double u = __dadd_rn(__dmul_rn(ae, inv_two_eb), 0.5);
+  double f = floor(u);
+  const double fr = __dsub_rn(u, f);
+  // the reciprocal product decides floor() unless the fraction is within
+  // 2^-40 of an integer (hb_interp.cuh: quantize_fast); NaN fails both tests
+  if (!(fabs(__dsub_rn(fr, 0.5)) < 0.5 - 0x1p-40) && !(u >= 200.5)) f = q_exact(ae, two_eb);
+  const double q = copysign(f, err);
+  const double r = __dadd_rn(p, __dmul_rn(two_eb, q));
+  const double stored = CAST32 ? (double)__double2float_rn(r) : r;
+  const bool ok = (f <= 127.0) && (fabs(__dsub_rn(o, stored)) <= eb);
+  *recon = ok ? r : o;
+  return ok ? (int)q + 128 : 0;
+}
+
+template <typename T, bool DEC, int K, bool LINEAR, bool INT, int TX, int CLS>
+__device__ __forceinline__ void tp_run_lv1(const TPassArgs& A, const double* tiles, int x0, int nx, int y, int z,
+                                           int yl, int zl, long long lin, long long slot, const T* o,
+                                           const uint8_t* cd, double eb, double two_eb, double inv_two_eb,
+                                           unsigned long long ocount, unsigned* shist, Acc& acc) {
+  const LevelGeom& g = A.g;
+  constexpr int odd2 = (CLS >> 2) & 1;
+  const long long P0 = 2ll * x0 + (CLS & 1), P1 = 2ll * y + ((CLS >> 1) & 1), P2 = 2ll * z + odd2;
+  const int kl0 = (int)g.kl[0], ks0 = (int)g.ks0;
+  uint8_t* sq = A.seq + slot;
+  const int n1 = cdim1(g, CLS, 1), n2p = (cdim1(g, CLS, 2) + 1) & ~1;
+  const int dst0 = n1 * n2p;
+  double* dp = CLS != 7 ? A.scr + (CLS - 1) * A.cstride + ((long long)x0 * n1 + y) * n2p + z : nullptr;
+  // axes of the class in ascending order, their tiles and tap strides
+  constexpr int ax0 = (CLS & 1) ? 0 : ((CLS & 2) ? 1 : 2);
+  constexpr int ax1 = K < 2 ? -1 : ((CLS & 1) ? ((CLS & 2) ? 1 : 2) : 2);
+  constexpr int ax2 = K < 3 ? -1 : 2;
+  constexpr int AX[3] = {ax0, ax1, ax2};
+  const double* tb[K];
+  int scls[K];
+#pragma unroll
+  for (int j = 0; j < K; j++) {
+    const int a = AX[j];
+    const Tile t = tile_of(a);
+    tb[j] = tiles + j * slot_of(TX) + yl * t.sy + zl + (a == 2);
+    scls[j] = (INT || a == 0) ? (LINEAR ? ST_MID : ST_CUBIC) : classify(a == 1 ? P1 : P2, g.D[a], 1, LINEAR);
+  }
+  T* op = DEC ? reinterpret_cast<T*>(A.out) + lin : nullptr;
+  unsigned h7 = 0, h8 = 0, h9 = 0;
+#pragma unroll
+  for (int i = 0; i < TX; i++) {
+    if (!INT && i >= nx) break;
+    double pv[K];
+    int ov[K];
+    double zpart = 0.0;
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+      const int a = AX[j];
+      const Tile t = tile_of(a);
+      int c = scls[j];
+      if (!INT && a == 0) c = classify(P0 + 2 * i, g.D[0], 1, LINEAR);
+      const double* q = tb[j] + i * t.sx;
+      if (DEC && a == 2) zpart = q[t.st];
+      if (INT) {
+        pv[j] = LINEAR ? apply_stencil(ST_MID, 0.0, q[t.st], q[2 * t.st], 0.0)
+                       : apply_stencil(ST_CUBIC, q[0], q[t.st], q[2 * t.st], q[3 * t.st]);
+        ov[j] = LINEAR ? 2 : 4;
+      } else {
+        pv[j] = apply_stencil(c, q[0], q[t.st], q[2 * t.st], q[3 * t.st]);
+        ov[j] = stencil_order(c);
+      }
+    }
+    const double pred = K == 1 ? pv[0] : (INT ? (K == 2 ? __dmul_rn(__dadd_rn(__dadd_rn(0.0, pv[0]), pv[1]), 0.5)
+                                                        : __ddiv_rn(__dadd_rn(__dadd_rn(__dadd_rn(0.0, pv[0]), pv[1]), pv[2]), 3.0))
+                                              : combine_axes(K, pv, ov));
+    double r;
+    if (!DEC) {
+      const double ov_ = (double)o[i];
+      const int code = quantize_lv1<sizeof(T) == 4>(ov_, pred, eb, two_eb, inv_two_eb, &r);
+      sq[(long long)i * ks0] = (uint8_t)code;
+      h7 += code == 127;
+      h8 += code == 128;
+      h9 += code == 129;
+      if ((unsigned)(code - 127) > 2u) {
+        atomicAdd(&shist[code], 1u);
+        if (code == 0) {
+          note_outlier(A.obm, (unsigned long long)(lin + (long long)i * kl0));
+          acc.bad |= !isfinite(ov_);
+        }
+      }
+    } else {
+      const int code = cd[i];
+      if (code != 0)
+        r = dequantize(pred, two_eb, code);
+      else
+        r = tp_outlier(A.oidx, A.oval, (unsigned long long)(lin + (long long)i * kl0), ocount, acc.bad);
+      T* opi = op + (long long)i * kl0;
+      if (!A.pairs) {
+        *opi = (T)r;
+        acc.nf |= !isfinite(r);
+      } else if (odd2) {  // one aligned store covers (z-1, z); the even-z classes write nothing
+        if (sizeof(T) == 4)
+          *reinterpret_cast<float2*>(opi - 1) = make_float2((float)zpart, (float)r);
+        else
+          *reinterpret_cast<double2*>(opi - 1) = make_double2(zpart, r);
+        acc.nf |= !isfinite(r) || !isfinite(zpart);
+      }
+    }
+    if (CLS != 7) dp[(long long)i * dst0] = r;
+  }
+  acc.h127 += h7;
+  acc.h128 += h8;
+  acc.h129 += h9;
+}
+
 // One CTA's tile of class k.  CLSC >= 0: that class is known at compile time
 // and interpolates along all its odd axes (multidim) -- every parity test,
 // tap stride and slot term folds; CLSC < 0: class and axes from the arguments
+// error bound, its reciprocal and the outlier count of the running launch
+__shared__ double sh_eb[3];
+__shared__ unsigned long long sh_ocount;
+
+template <bool DEC>
+__device__ __forceinline__ void sweep_consts(const TPassArgs& A) {
+  sh_eb[0] = A.st->eb;
+  sh_eb[1] = A.st->two_eb;
+  sh_eb[2] = __ddiv_rn(1.0, sh_eb[1]);
+  sh_ocount = DEC ? *A.ocount : 0;
+}
+
 // SWEEP: called from the persistent level-1 sweep (k_tsweep) -- the block
 // coordinates come from the work item, the mbarrier was initialised once and
 // completes phase `phase`, the histogram is flushed once per CTA at the end.
@@ -262,8 +406,8 @@ __device__ __forceinline__ bool tp_block(const TPassArgs& A, const TMaps& M, int
   const int yl = threadIdx.x >> 5, zl = threadIdx.x & 31;
   const int y = y0 + yl, z = z0 + zl;
   const int nx = min(TX, n0 - x0);
-  __shared__ double s_eb[3];
-  __shared__ unsigned long long s_ocount;
+  double* s_eb = sh_eb;
+  unsigned long long& s_ocount = sh_ocount;
   if (!SWEEP) {
     if (threadIdx.x == 0) {
       mbar_init(&bar, 1);
@@ -277,12 +421,7 @@ __device__ __forceinline__ bool tp_block(const TPassArgs& A, const TMaps& M, int
     if (!DEC)
       for (int i = threadIdx.x; i < 256; i += T_THREADS) shist[i] = 0;
     __syncthreads();
-  } else if (threadIdx.x == 0) {
-    s_eb[0] = A.st->eb;
-    s_eb[1] = A.st->two_eb;
-    s_eb[2] = __ddiv_rn(1.0, s_eb[1]);
-    s_ocount = DEC ? *A.ocount : 0;
-  }
+  }  // SWEEP: s_eb / s_ocount were set once at the start of the CTA (sweep_consts)
   if (threadIdx.x == 0) {
     unsigned bytes = 0;
     int m = AXM;
@@ -307,13 +446,26 @@ __device__ __forceinline__ bool tp_block(const TPassArgs& A, const TMaps& M, int
   T o[TX];
   uint8_t cd[TX];
   // element index and Eq. 3 slot of the run's first target (ordering.py:68-84)
-  const long long P0 = 2ll * x0 + odd0, P1 = 2ll * y + odd1, P2 = 2ll * z + odd2;
-  const long long sg = LV1 ? 1 : g.s;
-  const long long lin = ((P0 * sg) * g.d[1] + P1 * sg) * g.d[2] + P2 * sg;
-  long long slot = g.prefix + (P0 * g.D[1] + P1) * g.D[2] + P2 - ((P0 + 1) >> 1) * g.eyez;
-  if (!odd0) {
-    slot -= ((P1 + 1) >> 1) * g.ez;
-    if (!odd1) slot -= (P2 + 1) >> 1;
+  long long lin, slot;
+  if (LV1 && CLSC >= 0) {
+    // level 1, class fixed: both are affine in (x0, y, z) -- with P = 2u + odd
+    // and (P + 1) >> 1 = u + odd the Eq. 3 closed form collapses to
+    // slot = S0 + x0 * ks0 + y * (2 D2 - [!odd0] ez) + z * (2 - [!odd0 && !odd1])
+    const long long d12 = g.d[1] * g.d[2];
+    lin = odd0 * d12 + odd1 * g.d[2] + odd2 + (long long)x0 * g.kl[0] + (long long)(y * 2) * g.d[2] + 2 * z;
+    const long long s0 = g.prefix + odd0 * d12 + odd1 * g.d[2] + odd2 - odd0 * g.eyez -
+                         (odd0 ? 0 : odd1 * g.ez + (odd1 ? 0 : odd2));
+    slot = s0 + (long long)x0 * g.ks0 + (long long)y * (2 * g.d[2] - (odd0 ? 0 : g.ez)) +
+           (long long)z * (2 - (!odd0 && !odd1));
+  } else {
+    const long long P0 = 2ll * x0 + odd0, P1 = 2ll * y + odd1, P2 = 2ll * z + odd2;
+    const long long sg = LV1 ? 1 : g.s;
+    lin = ((P0 * sg) * g.d[1] + P1 * sg) * g.d[2] + P2 * sg;
+    slot = g.prefix + (P0 * g.D[1] + P1) * g.D[2] + P2 - ((P0 + 1) >> 1) * g.eyez;
+    if (!odd0) {
+      slot -= ((P1 + 1) >> 1) * g.ez;
+      if (!odd1) slot -= (P2 + 1) >> 1;
+    }
   }
   if (live) {
     if (!DEC) {
@@ -342,12 +494,21 @@ __device__ __forceinline__ bool tp_block(const TPassArgs& A, const TMaps& M, int
         full &= LINEAR ? (Phi + 1 < g.D[a]) : (Plo >= 3 && Phi + 3 < g.D[a]);
       }
   }
-  if (SWEEP) __syncthreads();  // s_eb / s_ocount
   const double eb = s_eb[0], two_eb = s_eb[1], inv_two_eb = s_eb[2];
   const unsigned long long ocount = s_ocount;
   Acc acc{0u, 0u, 0u, false, false};
   mbar_wait(&bar, phase);
-  if (live) {
+  if constexpr (LV1 && CLSC >= 0) {
+    full &= nx == TX;  // the interior loop has no x-extent check
+    if (live) {
+      if (full)
+        tp_run_lv1<T, DEC, K, LINEAR, true, TX, CLSC>(A, tiles, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb, two_eb,
+                                                      inv_two_eb, ocount, shist, acc);
+      else
+        tp_run_lv1<T, DEC, K, LINEAR, false, TX, CLSC>(A, tiles, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb, two_eb,
+                                                       inv_two_eb, ocount, shist, acc);
+    }
+  } else if (live) {
     if (full)
       tp_run<T, DEC, K, LINEAR, true, LV1, TX>(A, tiles, CLS, AXM, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb, two_eb, inv_two_eb, ocount,
                                       shist, acc);
@@ -386,7 +547,9 @@ __global__ void __launch_bounds__(T_THREADS, C0 >= 0 ? 4 : 2) k_tpass(const __gr
   extern __shared__ __align__(128) double tiles[];
   __shared__ unsigned shist[256];
   __shared__ __align__(8) uint64_t bar;
-  const int bx = (int)blockIdx.z / A.ncls, k = (int)blockIdx.z - bx * A.ncls;
+  // a single compile-time class per launch needs no class index
+  const int bx = (C0 >= 0 && C1 < 0) ? (int)blockIdx.z : (int)blockIdx.z / A.ncls;
+  const int k = (C0 >= 0 && C1 < 0) ? 0 : (int)blockIdx.z - bx * A.ncls;
   if constexpr (C0 < 0) {
     tp_block<T, DEC, K, LINEAR, LV1, -1, TX>(A, M, k, bx, tiles, shist, bar);
   } else {
@@ -430,6 +593,7 @@ constexpr int SKEW = 2;   // stages between dependent steps
 struct SweepArgs {
   TPassArgs A[3];  // step q: classes / maps of the step (plan_step)
   int nslab, nby, nbz, nitems;
+  int one;         // one item per CTA (grid = nitems) instead of a persistent loop
   int I[3];        // items per slab of step q
   unsigned* ticket;
   unsigned* done;  // [3][nslab] finished items per (step, slab)
@@ -450,7 +614,7 @@ __host__ __device__ __forceinline__ int stage_items(const SweepArgs& S, int t) {
 }
 
 template <typename T, bool DEC, bool LINEAR>
-__global__ void __launch_bounds__(T_THREADS, 3) k_tsweep(const __grid_constant__ SweepArgs S,
+__global__ void __launch_bounds__(T_THREADS, 4) k_tsweep(const __grid_constant__ SweepArgs S,
                                                         const __grid_constant__ SweepMaps SM) {
   extern __shared__ __align__(128) double tiles[];
   __shared__ unsigned shist[256];
@@ -465,11 +629,28 @@ __global__ void __launch_bounds__(T_THREADS, 3) k_tsweep(const __grid_constant__
     for (int i = threadIdx.x; i < 256; i += T_THREADS) shist[i] = 0;
   unsigned ph = 0;
   int t = 0, tstart = 0;
-  for (;;) {
-    if (threadIdx.x == 0) s_it = (int)atomicAdd(S.ticket, 1u);
+  // thread 0: the next ticket is fetched while the current item runs, and
+  // per step the prefix of predecessor slabs already seen complete is kept
+  unsigned nxt = 0;
+  int okp[3] = {-1, -1, -1};
+  if (threadIdx.x == 0) {
+    sweep_consts<DEC>(S.A[0]);
+    nxt = atomicAdd(S.ticket, 1u);
+  }
+  for (int n = 0; !S.one || n < 1; n++) {
+    if (threadIdx.x == 0) {
+      s_it = (int)nxt;
+      if (!S.one) nxt = atomicAdd(S.ticket, 1u);
+    }
     __syncthreads();
     const int it = s_it;
     if (it >= S.nitems) break;
+    if (S.one) {  // first stage at or after the item's lower bound: full stages hold Ifull items
+      const int full = S.I[0] + S.I[1] + S.I[2];
+      t = max(0, it / full - 2 * SKEW);
+      tstart = 0;
+      for (int u = 0; u < t; u++) tstart += stage_items(S, u);
+    }
     while (it >= tstart + stage_items(S, t)) tstart += stage_items(S, t++);
     int l = it - tstart, q = 0, j = t;
     if (t < S.nslab && l < S.I[0]) {
@@ -483,11 +664,13 @@ __global__ void __launch_bounds__(T_THREADS, 3) k_tsweep(const __grid_constant__
         q = 2, j = t - 2 * SKEW;
       }
     }
-    if (q > 0 && threadIdx.x == 0) {
+    if (q > 0 && threadIdx.x == 0 && okp[q] < min(S.nslab - 1, j + 1)) {
       const unsigned* d = S.done + (q - 1) * S.nslab;
       const unsigned need = (unsigned)S.I[q - 1];
-      for (int jj = max(0, j - 1); jj <= min(S.nslab - 1, j + 1); jj++)
+      const int hi = min(S.nslab - 1, j + 1);
+      for (int jj = okp[q] + 1; jj <= hi; jj++)
         while (ld_acquire(d + jj) < need) __nanosleep(32);
+      okp[q] = hi;
       // the class arrays written by those items are read through the async (TMA) proxy
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
@@ -701,13 +884,16 @@ unsigned* sweep_counters(const Launch& L) {
 }
 int sweep_slabs(const LevelGeom& g) { return (int)(((g.D[0] + 1) / 2 + SX - 1) / SX); }
 
-bool sweep_on() {
+// HB_SWEEP: 0 = seven per-class launches, 1 = sweep with one item per CTA,
+// 2 = persistent sweep (one CTA per resident slot looping over tickets)
+int sweep_mode() {
   static const int v = [] {
     const char* e = getenv("HB_SWEEP");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;
   }();
-  return v != 0;
+  return v;
 }
+bool sweep_on() { return sweep_mode() != 0; }
 
 template <typename T, bool DEC, bool LINEAR>
 bool launch_sweep(const Launch& base, cudaStream_t s, int* launches) {
@@ -741,7 +927,8 @@ bool launch_sweep(const Launch& base, cudaStream_t s, int* launches) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tsweep<T, DEC, LINEAR>, T_THREADS, smem);
     if (per_sm < 1) per_sm = 1;
   }
-  const int grid = std::min(S.nitems, kSMs * per_sm);
+  S.one = sweep_mode() == 1;
+  const int grid = S.one ? S.nitems : std::min(S.nitems, kSMs * per_sm);
   k_tsweep<T, DEC, LINEAR><<<grid, T_THREADS, smem, s>>>(S, SM);
   (*launches) += 2;
   return true;

@@ -9,6 +9,8 @@ others so none of them ships untested:
   HB_NO_GRAPHS       no CUDA-graph capture/replay of the compress tail / decompress
   HB_SERIAL_TUNE     tuner and level passes on one stream (no overlap)
   HB_MARCH=1         axis-0 marching level kernel (k_march.cu) for multidim 3D levels
+  HB_SWEEP=2 / 1     level 1 as one slab-ordered sweep (persistent / one item per CTA)
+                     instead of the seven per-class TMA passes
 """
 import os
 import subprocess
@@ -29,6 +31,8 @@ VARIANTS = {
     "no-graphs": {"HB_NO_GRAPHS": "1"},
     "serial-tune": {"HB_SERIAL_TUNE": "1"},
     "march": {"HB_MARCH": "1"},
+    "sweep": {"HB_SWEEP": "2"},
+    "sweep-one": {"HB_SWEEP": "1"},
 }
 
 
