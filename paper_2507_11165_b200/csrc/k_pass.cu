@@ -280,7 +280,7 @@ __device__ __forceinline__ int quantize_lv1(double o, double p, double eb, doubl
   return ok ? (int)q + 128 : 0;
 }
 
-template <typename T, bool DEC, int K, bool LINEAR, bool INT, int TX, int CLS>
+template <typename T, bool DEC, int K, bool LINEAR, bool INT, int TX, int CLS, bool LV1 = true>
 __device__ __forceinline__ void tp_run_lv1(const TPassArgs& A, const double* tiles, int x0, int nx, int y, int z,
                                            int yl, int zl, long long lin, long long slot, const T* o,
                                            const uint8_t* cd, double eb, double two_eb, double inv_two_eb,
@@ -293,6 +293,11 @@ __device__ __forceinline__ void tp_run_lv1(const TPassArgs& A, const double* til
   const int n1 = cdim1(g, CLS, 1), n2p = (cdim1(g, CLS, 2) + 1) & ~1;
   const int dst0 = n1 * n2p;
   double* dp = CLS != 7 ? A.scr + (CLS - 1) * A.cstride + ((long long)x0 * n1 + y) * n2p + z : nullptr;
+  // levels >= 2: the target is also a point of the next level's lattice (E)
+  const long long sg = LV1 ? 1 : g.s;
+  double* ep = LV1 ? nullptr
+                   : A.E + ((P0 * sg) >> 1) * g.Ed[1] * g.Ed[2] + ((P1 * sg) >> 1) * g.Ed[2] + ((P2 * sg) >> 1);
+  const long long ke0 = g.ke[0];
   // axes of the class in ascending order, their tiles and tap strides
   constexpr int ax0 = (CLS & 1) ? 0 : ((CLS & 2) ? 1 : 2);
   constexpr int ax1 = K < 2 ? -1 : ((CLS & 1) ? ((CLS & 2) ? 1 : 2) : 2);
@@ -357,7 +362,9 @@ __device__ __forceinline__ void tp_run_lv1(const TPassArgs& A, const double* til
       else
         r = tp_outlier(A.oidx, A.oval, (unsigned long long)(lin + (long long)i * kl0), ocount, acc.bad);
       T* opi = op + (long long)i * kl0;
-      if (!A.pairs) {
+      if (!LV1) {
+        // not an output point yet: the value lives on in E
+      } else if (!A.pairs) {
         *opi = (T)r;
         acc.nf |= !isfinite(r);
       } else if (odd2) {  // one aligned store covers (z-1, z); the even-z classes write nothing
@@ -369,6 +376,7 @@ __device__ __forceinline__ void tp_run_lv1(const TPassArgs& A, const double* til
       }
     }
     if (CLS != 7) dp[(long long)i * dst0] = r;
+    if (!LV1) ep[i * ke0] = r;
   }
   acc.h127 += h7;
   acc.h128 += h8;
@@ -378,6 +386,8 @@ __device__ __forceinline__ void tp_run_lv1(const TPassArgs& A, const double* til
 // One CTA's tile of class k.  CLSC >= 0: that class is known at compile time
 // and interpolates along all its odd axes (multidim) -- every parity test,
 // tap stride and slot term folds; CLSC < 0: class and axes from the arguments
+#define AXM_OF(c) (c)  // class-specialised bodies are multidim: every odd axis interpolates
+
 // error bound, its reciprocal and the outlier count of the running launch
 __shared__ double sh_eb[3];
 __shared__ unsigned long long sh_ocount;
@@ -498,15 +508,15 @@ __device__ __forceinline__ bool tp_block(const TPassArgs& A, const TMaps& M, int
   const unsigned long long ocount = s_ocount;
   Acc acc{0u, 0u, 0u, false, false};
   mbar_wait(&bar, phase);
-  if constexpr (LV1 && CLSC >= 0) {
+  if constexpr (CLSC >= 0 && (CLSC == AXM_OF(CLSC))) {
     full &= nx == TX;  // the interior loop has no x-extent check
     if (live) {
       if (full)
-        tp_run_lv1<T, DEC, K, LINEAR, true, TX, CLSC>(A, tiles, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb, two_eb,
-                                                      inv_two_eb, ocount, shist, acc);
+        tp_run_lv1<T, DEC, K, LINEAR, true, TX, CLSC, LV1>(A, tiles, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb,
+                                                           two_eb, inv_two_eb, ocount, shist, acc);
       else
-        tp_run_lv1<T, DEC, K, LINEAR, false, TX, CLSC>(A, tiles, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb, two_eb,
-                                                       inv_two_eb, ocount, shist, acc);
+        tp_run_lv1<T, DEC, K, LINEAR, false, TX, CLSC, LV1>(A, tiles, x0, nx, y, z, yl, zl, lin, slot, o, cd, eb,
+                                                            two_eb, inv_two_eb, ocount, shist, acc);
     }
   } else if (live) {
     if (full)
@@ -940,13 +950,13 @@ template <typename T, bool DEC, bool LINEAR, bool LV1>
 bool run_passes(const Launch& base, int cfg, cudaStream_t s, int* launches) {
   Launch L[7] = {base, base, base, base, base, base, base};
   int K[3];
-  if ((cfg & 2) == 0 && !LV1) {  // multidim, small levels: one launch per dependency step
+  if ((cfg & 2) == 0 && !LV1) {  // multidim, small levels: one launch per dependency step, class-specialised bodies
     const int c1[3] = {1, 2, 4}, c2[3] = {3, 5, 6}, c3[1] = {7};
     if (!plan_step(L[0], 1, c1, c1, 3) || !plan_step(L[1], 2, c2, c2, 3) || !plan_step(L[2], 3, c3, c3, 1))
       return false;
-    launch_step<T, DEC, 1, LINEAR, LV1>(L[0], s, launches);
-    launch_step<T, DEC, 2, LINEAR, LV1>(L[1], s, launches);
-    launch_step<T, DEC, 3, LINEAR, LV1>(L[2], s, launches);
+    launch_step<T, DEC, 1, LINEAR, LV1, 1, 2, 4>(L[0], s, launches);
+    launch_step<T, DEC, 2, LINEAR, LV1, 3, 5, 6>(L[1], s, launches);
+    launch_step<T, DEC, 3, LINEAR, LV1, 7>(L[2], s, launches);
     return true;
   }
   if ((cfg & 2) == 0 && LV1 && sweep_on() && launch_sweep<T, DEC, LINEAR>(base, s, launches)) return true;
