@@ -787,7 +787,7 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
   const size_t o_seq = L.take(N + 128);
   const size_t o_obm = L.take(cdiv(N, 32) * 4 + 64);
   const size_t o_org = L.take(org.size() * 8 + 8);
-  const size_t o_trials = L.take(tune_global ? tune_global_bytes(tp.bn) : (size_t)2 * 4 * tp.nb * tp.bn * 8);
+  const size_t o_trials = L.take(tune_global ? tune_global_bytes(tp.bn) : tune_ws_bytes(tp));
   const size_t o_berr = L.take((size_t)4 * tp.nb * 8);
   const size_t o_arch = L.take(bound + N / 4 + 4096);
   const unsigned long long hf_max = 274 + N + 64;
@@ -937,8 +937,7 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
     ctx->mark_on("anchors", s2);
     uint8_t* pc = ctx->pinned + 4096 + 512;
     for (int level = tp.top; level >= 1; level--) {
-      launch_tune_level(tp, dfield, prec, dims, d_org, level, trials, berr, st, s, &nl);
-      launch_tune_select(tp, level, berr, st, s, &nl, pc);
+      launch_tune_level(tp, dfield, prec, dims, d_org, level, trials, berr, st, s, &nl, pc);
       CU(cudaEventRecord(ctx->ev_tune[level], s));
     }
     ctx->mark("tune");
@@ -976,7 +975,6 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
   } else {
     for (int level = tp.top; level >= 1; level--) {
       launch_tune_level(tp, dfield, prec, dims, d_org, level, trials, berr, st, s, &nl);
-      launch_tune_select(tp, level, berr, st, s, &nl);
     }
   }
   if (!overlap) ctx->mark("tune");

@@ -101,12 +101,12 @@ struct TunePlan {
   unsigned long long bn;
 };
 bool tune_supported(const TunePlan& p);
+// one launch per level; the CTA that finishes last runs the select (tuning.py:135-140)
+// and publishes the level's config byte (also to host_cfg, mapped pinned memory)
+size_t tune_ws_bytes(const TunePlan& p);
 void launch_tune_level(const TunePlan& p, const void* field, int prec, const uint64_t dims[3],
                        const unsigned long long* origins, int level, double* trials, double* berr, DevState* st,
-                       cudaStream_t s, int* launches);
-void launch_tune_select(const TunePlan& p, int level, const double* berr, DevState* st, cudaStream_t s,
-                        int* launches,
-                        uint8_t* host_cfg = nullptr);
+                       cudaStream_t s, int* launches, uint8_t* host_cfg = nullptr);
 // whole-field blocks too large for shared memory
 size_t tune_global_bytes(unsigned long long bn);
 int launch_tune_global(const void* field, int prec, const uint64_t dims[3], int top, uint8_t* scratch,

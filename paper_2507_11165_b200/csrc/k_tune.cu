@@ -128,10 +128,58 @@ __device__ double pw_combine(int n, const double* leaf, int* cursor) {
   return __dadd_rn(a, b);
 }
 
+// a / b for 0 <= a < 2^22, 0 < b < 2^12 through the float reciprocal rb = 1/b
+// (one correction step each way makes it exact)
+__device__ __forceinline__ int qdiv(int a, int b, float rb) {
+  int q = __float2int_rz(__int2float_rn(a) * rb);
+  int r = a - q * b;
+  if (r < 0) q--, r += b;
+  if (r >= b) q++;
+  return q;
+}
+
+// tuning.py:135-140 for one level, run by the first warp of the CTA that
+// finishes the level last (k_tune_level): Neumaier sum of the block errors per
+// config, (err, index) argmin, winner handed to the next level.
+__device__ void tune_select(int nb, int level, const double* berr, DevState* st, uint8_t* host_cfg) {
+  __shared__ double e[4];
+  const int ci = threadIdx.x;
+  if (ci < 4) {
+    const double* x = berr + ci * nb;
+    double f = __dadd_rn(0.0, __ldcg(&x[0])), c = 0.0;  // sum() starts from int 0
+    for (int i = 1; i < nb; i++) {
+      const double xi = __ldcg(&x[i]);
+      const double t = __dadd_rn(f, xi);
+      if (fabs(f) >= fabs(xi))
+        c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), xi));
+      else
+        c = __dadd_rn(c, __dadd_rn(__dsub_rn(xi, t), f));
+      f = t;
+    }
+    if (c != 0.0 && isfinite(c)) f = __dadd_rn(f, c);
+    e[ci] = f;
+    st->tune_errs[(level - 1) * 4 + ci] = f;
+  }
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    int best = 0;
+    for (int i = 1; i < 4; i++)
+      if (e[i] < e[best]) best = i;
+    st->tune_winner[level - 1] = best;
+    st->cfg[level - 1] = c_choice[best];
+    __threadfence();
+    if (host_cfg) {  // mapped pinned memory: the host reads it once an event after this kernel completes
+      host_cfg[level - 1] = c_choice[best];
+      __threadfence_system();
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(TUNE_THREADS)
     k_tune_level(const T* __restrict__ field, long long fd1, long long fd2, const unsigned long long* origins, int nb,
-                 int b0, int b1, int b2, int top, int level, double* trials, double* berr, DevState* st) {
+                 int b0, int b1, int b2, int top, int level, double* trials, double* berr, DevState* st,
+                 T* borig, unsigned* done, uint8_t* host_cfg) {
   extern __shared__ double tsm[];
   const int bn = b0 * b1 * b2;
   double* g = tsm;
@@ -141,11 +189,19 @@ __global__ void __launch_bounds__(TUNE_THREADS)
   __shared__ int lstart[160], llen[160];
   __shared__ int nleaf;
   const int ci = blockIdx.x / nb, b = blockIdx.x % nb;
-  const unsigned long long ox = origins[3 * b], oy = origins[3 * b + 1], oz = origins[3 * b + 2];
-  // original block values (tuning.py:111-112)
-  for (int i = threadIdx.x; i < bn; i += blockDim.x) {
-    const int z = i % b2, y = (i / b2) % b1, x = i / (b2 * b1);
-    orig[i] = field[((ox + x) * fd1 + oy + y) * fd2 + oz + z];
+  // original block values (tuning.py:111-112): gathered from the field at the
+  // top level (and kept compact in borig), read back contiguously below it
+  if (level == top) {
+    const unsigned long long ox = origins[3 * b], oy = origins[3 * b + 1], oz = origins[3 * b + 2];
+    const float r2 = 1.0f / (float)b2, r12 = 1.0f / (float)(b1 * b2);
+    for (int i = threadIdx.x; i < bn; i += blockDim.x) {
+      const int x = qdiv(i, b1 * b2, r12), yz = i - x * b1 * b2, y = qdiv(yz, b2, r2), z = yz - y * b2;
+      const T v = field[((ox + x) * fd1 + oy + y) * fd2 + oz + z];
+      orig[i] = v;
+      if (ci == 0) borig[(size_t)b * bn + i] = v;
+    }
+  } else {
+    for (int i = threadIdx.x; i < bn; i += blockDim.x) orig[i] = borig[(size_t)b * bn + i];
   }
   // state carried from the previous level's winner (tuning.py:140)
   const size_t set_stride = (size_t)4 * nb * bn;
@@ -169,11 +225,14 @@ __global__ void __launch_bounds__(TUNE_THREADS)
   for (int t = 0; t < nss; t++) {
     const SubStep& S = ss[t];
     const int n = S.count[0] * S.count[1] * S.count[2];
+    const int c12 = S.count[1] * S.count[2];
+    const float r2 = 1.0f / (float)S.count[2], r12 = 1.0f / (float)c12;
     for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
       int c[3];
-      c[2] = S.start[2] + (idx % S.count[2]) * S.step[2];
-      c[1] = S.start[1] + ((idx / S.count[2]) % S.count[1]) * S.step[1];
-      c[0] = S.start[0] + (idx / (S.count[2] * S.count[1])) * S.step[0];
+      const int q0 = qdiv(idx, c12, r12), rem = idx - q0 * c12, q1 = qdiv(rem, S.count[2], r2);
+      c[2] = S.start[2] + (rem - q1 * S.count[2]) * S.step[2];
+      c[1] = S.start[1] + q1 * S.step[1];
+      c[0] = S.start[0] + q0 * S.step[0];
       const int lin = (c[0] * b1 + c[1]) * b2 + c[2];
       double pv[3];
       int ov[3];
@@ -240,40 +299,19 @@ __global__ void __launch_bounds__(TUNE_THREADS)
   }
   double* dst = trials + (size_t)(level & 1) * set_stride + ((size_t)ci * nb + b) * bn;
   for (int i = threadIdx.x; i < bn; i += blockDim.x) dst[i] = g[i];
-  if (threadIdx.x == 0) berr[ci * nb + b] = total;
-}
-
-// tuning.py:135-140
-__global__ void k_tune_select(int nb, int level, const double* berr, DevState* st, uint8_t* host_cfg) {
-  __shared__ double e[4];
-  const int ci = threadIdx.x;
-  if (ci < 4) {
-    const double* x = berr + ci * nb;
-    double f = __dadd_rn(0.0, x[0]), c = 0.0;  // sum() starts from int 0
-    for (int i = 1; i < nb; i++) {
-      const double t = __dadd_rn(f, x[i]);
-      if (fabs(f) >= fabs(x[i]))
-        c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x[i]));
-      else
-        c = __dadd_rn(c, __dadd_rn(__dsub_rn(x[i], t), f));
-      f = t;
-    }
-    if (c != 0.0 && isfinite(c)) f = __dadd_rn(f, c);
-    e[ci] = f;
-    st->tune_errs[(level - 1) * 4 + ci] = f;
-  }
+  // the CTA that finishes the level last selects its config (no extra launch)
+  __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    int best = 0;
-    for (int i = 1; i < 4; i++)
-      if (e[i] < e[best]) best = i;
-    st->tune_winner[level - 1] = best;
-    st->cfg[level - 1] = c_choice[best];
-    if (host_cfg) {  // mapped pinned memory: the host reads it once an event after this kernel completes
-      host_cfg[level - 1] = c_choice[best];
-      __threadfence_system();
-    }
+    berr[ci * nb + b] = total;
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < 32) tune_select(nb, level, berr, st, host_cfg);
+  if (threadIdx.x == 0) *done = 0;  // ready for the next level / call
 }
 
 static size_t tune_smem(const TunePlan& p, int prec) {
@@ -282,27 +320,30 @@ static size_t tune_smem(const TunePlan& p, int prec) {
 
 bool tune_supported(const TunePlan& p) { return tune_smem(p, 8) <= 200 * 1024; }
 
+size_t tune_ws_bytes(const TunePlan& p) {
+  // trials (two level sets of 4 configs) | compact block originals | level counter
+  return (size_t)2 * 4 * p.nb * p.bn * 8 + (size_t)p.nb * p.bn * 8 + 64;
+}
+
 void launch_tune_level(const TunePlan& p, const void* field, int prec, const uint64_t dims[3],
                        const unsigned long long* origins, int level, double* trials, double* berr, DevState* st,
-                       cudaStream_t s, int* launches) {
+                       cudaStream_t s, int* launches, uint8_t* host_cfg) {
   const size_t smem = tune_smem(p, prec);
+  double* borig = trials + (size_t)2 * 4 * p.nb * p.bn;
+  unsigned* done = reinterpret_cast<unsigned*>(borig + (size_t)p.nb * p.bn);
+  if (level == p.top) cudaMemsetAsync(done, 0, sizeof(unsigned), s);
   if (prec == 4) {
     cudaFuncSetAttribute(k_tune_level<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_tune_level<float><<<4 * p.nb, TUNE_THREADS, smem, s>>>((const float*)field, dims[1], dims[2], origins, p.nb,
                                                              p.shape[0], p.shape[1], p.shape[2], p.top, level, trials,
-                                                             berr, st);
+                                                             berr, st, reinterpret_cast<float*>(borig), done,
+                                                             host_cfg);
   } else {
     cudaFuncSetAttribute(k_tune_level<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_tune_level<double><<<4 * p.nb, TUNE_THREADS, smem, s>>>((const double*)field, dims[1], dims[2], origins, p.nb,
                                                               p.shape[0], p.shape[1], p.shape[2], p.top, level,
-                                                              trials, berr, st);
+                                                              trials, berr, st, borig, done, host_cfg);
   }
-  (*launches)++;
-}
-
-void launch_tune_select(const TunePlan& p, int level, const double* berr, DevState* st, cudaStream_t s,
-                        int* launches, uint8_t* host_cfg) {
-  k_tune_select<<<1, 32, 0, s>>>(p.nb, level, berr, st, host_cfg);
   (*launches)++;
 }
 
