@@ -203,8 +203,14 @@ def run_probe(args):
     out = torch.empty(hb.compress_bound(f.dims, 4), dtype=torch.uint8, device="cuda")
     hb.compress_device(f, spec, args.mode, out=out)
     torch.cuda.synchronize()
-    os.environ["HB_NCU_RANGE"] = "level1"
-    hb.compress_device(f, spec, args.mode, out=out)
+    # HB_PROBE_RANGE=0: no profiler range (a launch list of the whole step;
+    # cudaProfilerStop would end an ncu session that profiles from the start)
+    if os.environ.get("HB_PROBE_RANGE", "1") != "0":
+        os.environ["HB_NCU_RANGE"] = "level1"
+    a = hb.compress_device(f, spec, args.mode, out=out)
+    torch.cuda.synchronize()
+    os.environ.pop("HB_NCU_RANGE", None)
+    hb.decompress_device(a, f.dims, np.float32)
     torch.cuda.synchronize()
 
 

@@ -1155,7 +1155,7 @@ int hb_decompress(hb_ctx* ctx, const void* archive, size_t len, void* field_out,
   auto seq_all = [&]() -> int {
     CU(cudaMemsetAsync(st, 0, sizeof(DevState), s));
     CU(cudaMemsetAsync(lb, 0, lbn * 8 * 12, s));
-    CU(cudaMemsetAsync(base + o_hd, 0, hd_bytes, s));
+    // (the Huffman decoder zeroes the part of its workspace that needs it)
     ctx->nev = 0;
     ctx->mark("start");
     k_set_cfg_eb<<<1, 1, 0, s>>>(st, I.cfg[0], I.cfg[1], I.cfg[2], I.cfg[3], I.eb);
@@ -1558,7 +1558,7 @@ int hb_stage_decode(hb_ctx* ctx, int stage, const void* in, size_t n, void* out,
   int nl = 0;
   CU(cudaMemsetAsync(st, 0, sizeof(DevState), s));
   CU(cudaMemsetAsync(lb, 0, lbn * 8 * 12, s));
-  CU(cudaMemsetAsync(base + o_hd, 0, hd_bytes, s));
+  // (the Huffman decoder zeroes the part of its workspace that needs it)
   if (n) CU(cudaMemcpyAsync(base + o_in, in, n, cudaMemcpyDefault, s));
   k_set_u64<<<1, 1, 0, s>>>(&st->scratch[2], n);
   nl++;

@@ -1223,7 +1223,6 @@ void launch_bit_encode(const uint8_t* in, const unsigned long long* n_dev, int w
 
 constexpr int HD_S = 512;        // bits per subsequence
 constexpr int HD_K = 12;         // LUT bits
-constexpr int HD_PASSES = 4;
 
 struct HDTables {
   int ok;
@@ -1784,64 +1783,6 @@ __global__ void __launch_bounds__(256) k_hd_first(const uint8_t* rec, const HDTa
   }
 }
 
-// pass p: read buffers (p-1)&1, write p&1
-__global__ void __launch_bounds__(256) k_hd_pass(int p, const uint8_t* rec, const HDTables* T, HDWork W) {
-  __shared__ HDShared S;
-  if (!T->ok) return;
-  const int rd = (p - 1) & 1, wr = p & 1;
-  const unsigned long long nsub = T->nsub;
-  if (p > 1 && !W.changed[p - 1]) {  // converged: carry the state forward
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nsub;
-         i += (unsigned long long)gridDim.x * blockDim.x) {
-      W.s[wr][i] = W.s[rd][i];
-      W.e[wr][i] = W.e[rd][i];
-      W.c[wr][i] = W.c[rd][i];
-    }
-    return;
-  }
-  hd_load_shared(&S, T);
-  __syncthreads();
-  const uint8_t* pay = rec + T->pay_off;
-  bool ch = false;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nsub;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long want = i == 0 ? 0ull : W.e[rd][i - 1];
-    if (want == W.s[rd][i] || want == ~0ull) {
-      W.s[wr][i] = W.s[rd][i];
-      W.e[wr][i] = W.e[rd][i];
-      W.c[wr][i] = W.c[rd][i];
-    } else {
-      unsigned long long e = want;
-      long long c = 0;
-      bool done = false;
-      if (p == 1 && W.e[rd][i] != ~0ull && want >= i * HD_S) {
-        // decode from the true start until it meets a codeword start of the
-        // first pass (from there both decodes are identical)
-        unsigned long long ps;
-        const unsigned long long bm = W.bmask[i];
-        const long long k = hd_decode<false, false, true>(*T, &S, pay, want, (i + 1) * HD_S, &ps, nullptr, nullptr,
-                                                          i * HD_S, bm);
-        if (k >= 0) {
-          const unsigned long long q = ps - i * HD_S;
-          const unsigned before = __popcll(bm & ((1ull << q) - 1));
-          W.s[wr][i] = want;
-          W.e[wr][i] = W.e[rd][i];
-          W.c[wr][i] = W.c[rd][i] - before + (unsigned)k;
-          done = true;
-        }
-      }
-      if (!done) {
-        if (want < (i + 1) * HD_S) c = hd_decode<false>(*T, &S, pay, want, (i + 1) * HD_S, &e, nullptr);
-        W.s[wr][i] = want;
-        W.e[wr][i] = c < 0 ? ~0ull : e;
-        W.c[wr][i] = c < 0 ? 0u : (unsigned)c;
-      }
-      ch = true;
-    }
-  }
-  if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) W.changed[p] = 1;
-}
-
 // exclusive scan of counts (decoupled look-back over 2048-entry tiles staged
 // through shared memory: coalesced loads and stores)
 constexpr int HS_TILE = 2048;
@@ -2053,7 +1994,7 @@ __global__ void __launch_bounds__(256) k_hd_fix(const uint8_t* rec, const HDTabl
   if (blockIdx.x == 0 && threadIdx.x == 0) W.changed[HD_ROUNDS + 1] = 1;  // not converged: serial sweep
 }
 
-// serial fallback when HD_PASSES did not converge (adversarial streams)
+// serial fallback when the fix-up rounds did not converge (adversarial streams)
 __global__ void k_hd_serial(const uint8_t* rec, const HDTables* T, HDWork W, int fin) {
   if (!T->ok || !W.changed[HD_ROUNDS + 1]) return;
   const unsigned long long nsub = T->nsub;
@@ -2077,7 +2018,7 @@ __global__ void k_hd_serial(const uint8_t* rec, const HDTables* T, HDWork W, int
 
 size_t huffman_decode_ws_bytes(unsigned long long max_payload_bytes) {
   const unsigned long long nsub = cdiv(max_payload_bytes * 8, HD_S) + 1;
-  return sizeof(HDTables) + 256 + nsub * (8 * 2 + 8 * 2 + 4 * 2 + 8 + 8) + 64 + 256 + (HD_ROUNDS + 8) * 4;
+  return sizeof(HDTables) + 256 + ((HD_ROUNDS + 8) * 4 + 256) + nsub * (8 * 2 + 8 * 2 + 4 * 2 + 8 + 8) + 64;
 }
 
 void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long* len_dev, unsigned long long n,
@@ -2088,6 +2029,9 @@ void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long*
   HDTables* T = reinterpret_cast<HDTables*>(p);
   p += (sizeof(HDTables) + 255) & ~255ull;
   HDWork W;
+  W.changed = reinterpret_cast<int*>(p);  // HD_ROUNDS + 4 ints (flags, barrier): zeroed here, the rest of the
+  cudaMemsetAsync(W.changed, 0, (HD_ROUNDS + 8) * 4, s);  // workspace is written before it is read
+  p += ((HD_ROUNDS + 8) * 4 + 255) & ~255ull;
   for (int b = 0; b < 2; b++) {
     W.s[b] = reinterpret_cast<unsigned long long*>(p);
     p += nsub_max * 8;
@@ -2102,7 +2046,6 @@ void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long*
     W.c[b] = reinterpret_cast<unsigned*>(p);
     p += nsub_max * 4;
   }
-  W.changed = reinterpret_cast<int*>(p);  // HD_ROUNDS + 4 ints (flags, barrier), zeroed by the caller
   k_hd_setup<<<1, 256, 0, s>>>(hf_rec, len_dev, n, max_out, T, st);
   (*launches)++;
   const unsigned g = persist_grid(cdiv(nsub_max, 256));
