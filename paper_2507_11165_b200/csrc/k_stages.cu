@@ -1221,11 +1221,16 @@ void launch_bit_encode(const uint8_t* in, const unsigned long long* n_dev, int w
 // frequent symbol has the 1-bit code "0" (smooth fields) runs of zero bits
 // are consumed with one clz.  Output goes out in aligned 16-byte stores.
 
-constexpr int HD_S = 512;        // bits per subsequence
+// bits per subsequence: 512 for large payloads (throughput), down to 128 when
+// 512-bit subsequences would not fill the GPU (a thread's decode chain is the
+// latency of a small stream) -- chosen per stream in k_hd_setup
+constexpr int HD_S_MAX = 512, HD_S_MIN = 128;
+constexpr unsigned long long HD_FILL = 148ull * 4 * 256;  // subsequences that fill the GPU
 constexpr int HD_K = 12;         // LUT bits
 
 struct HDTables {
   int ok;
+  unsigned S;  // bits per subsequence
   int maxlen, K;
   int run_sym;  // symbol with the 1-bit code "0", or -1
   unsigned long long nsym, nbits, pay_off, pay_len, nsub;
@@ -1265,7 +1270,7 @@ struct HDWork {  // per pass: start, end, count per subsequence
 // stages.py:332-368: record checks, Kraft, canonical tables, LUT (parallel)
 __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsigned long long* len_dev,
                                                   unsigned long long n_expect, unsigned long long max_out,
-                                                  HDTables* T, DevState* st) {
+                                                  unsigned long long nsub_cap, HDTables* T, DevState* st) {
   __shared__ int ok_sh, cnt[257], maxlen_sh;
   __shared__ uint8_t len[256];
   // shared copies of the canonical tables for the parallel LUT builds below
@@ -1353,7 +1358,11 @@ __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsi
       for (int L = 0; L < 64; L++) T->first_rank[L] = s_rank[L], T->count[L] = s_count[L], T->first_code[L] = s_first[L];
       T->maxlen = maxlen;
       T->K = maxlen < HD_K ? maxlen : HD_K;
-      T->nsub = cdiv(T->nbits, HD_S);
+      unsigned S = HD_S_MAX;
+      while (S > HD_S_MIN && T->nbits / S < HD_FILL && cdiv(T->nbits, (unsigned long long)(S / 2)) + 1 <= nsub_cap)
+        S >>= 1;
+      T->S = S;
+      T->nsub = cdiv(T->nbits, (unsigned long long)S);
     }
     ok_sh = good;
   }
@@ -1769,12 +1778,13 @@ __global__ void __launch_bounds__(256) k_hd_first(const uint8_t* rec, const HDTa
   hd_load_shared(&S, T);
   __syncthreads();
   const unsigned long long nsub = T->nsub;
+  const unsigned long long SB = T->S;
   const uint8_t* pay = rec + T->pay_off;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nsub;
        i += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long s0 = i * HD_S;
+    const unsigned long long s0 = i * SB;
     unsigned long long e, m = 0;
-    const long long c = hd_decode<false, true>(*T, &S, pay, s0, s0 + HD_S, &e, nullptr, &m);
+    const long long c = hd_decode<false, true>(*T, &S, pay, s0, s0 + SB, &e, nullptr, &m);
     W.bmask[i] = m;
     W.s[0][i] = s0;
     W.e[0][i] = c < 0 ? ~0ull : e;  // error end never matches a successor start
@@ -1844,6 +1854,7 @@ __global__ void __launch_bounds__(256, 4) k_hd_emit(const uint8_t* rec, const HD
   hd_load_shared(&S, T);
   __syncthreads();
   const unsigned long long nsub = T->nsub;
+  const unsigned long long SB = T->S;
   const uint8_t* pay = rec + T->pay_off;
   unsigned zeros = 0;
   bool bad = false;
@@ -1858,7 +1869,7 @@ __global__ void __launch_bounds__(256, 4) k_hd_emit(const uint8_t* rec, const HD
     OutWriter ow;
     ow.init(out, W.off[i], T->run_sym >= 0 ? T->run_sym : 0);
     unsigned long long e;
-    const long long c = hd_decode<true>(*T, &S, pay, s0, (i + 1) * HD_S, &e, &ow);
+    const long long c = hd_decode<true>(*T, &S, pay, s0, (i + 1) * SB, &e, &ow);
     ow.finish();
     zeros += ow.zeros;
     bad |= c < 0;
@@ -1903,6 +1914,7 @@ __global__ void __launch_bounds__(256) k_hd_fix(const uint8_t* rec, const HDTabl
   hd_load_shared(&S, T);
   __syncthreads();
   const unsigned long long nsub = T->nsub;
+  const unsigned long long SB = T->S;
   const uint8_t* pay = rec + T->pay_off;
   unsigned* bar = reinterpret_cast<unsigned*>(W.changed + HD_ROUNDS + 2);
   volatile unsigned long long* E = W.e[0];
@@ -1910,7 +1922,7 @@ __global__ void __launch_bounds__(256) k_hd_fix(const uint8_t* rec, const HDTabl
   auto redecode = [&](unsigned long long i, unsigned long long want) {
     unsigned long long e = want;
     long long c = 0;
-    if (want < (i + 1) * HD_S) c = hd_decode<false>(*T, &S, pay, want, (i + 1) * HD_S, &e, nullptr);
+    if (want < (i + 1) * SB) c = hd_decode<false>(*T, &S, pay, want, (i + 1) * SB, &e, nullptr);
     W.c[0][i] = c < 0 ? 0u : (unsigned)c;
     W.s[0][i] = want;
     __threadfence();
@@ -1928,13 +1940,13 @@ __global__ void __launch_bounds__(256) k_hd_fix(const uint8_t* rec, const HDTabl
     const unsigned long long s0 = W.s[0][i];
     if (want == s0 || want == ~0ull) continue;
     bool done = false;
-    if (E1[i] != ~0ull && want >= i * HD_S) {
+    if (E1[i] != ~0ull && want >= i * SB) {
       unsigned long long ps;
       const unsigned long long bm = W.bmask[i];
-      const long long k = hd_decode<false, false, true>(*T, &S, pay, want, (i + 1) * HD_S, &ps, nullptr, nullptr,
-                                                        i * HD_S, bm);
+      const long long k = hd_decode<false, false, true>(*T, &S, pay, want, (i + 1) * SB, &ps, nullptr, nullptr,
+                                                        i * SB, bm);
       if (k >= 0) {
-        const unsigned long long q = ps - i * HD_S;
+        const unsigned long long q = ps - i * SB;
         const unsigned before = __popcll(bm & ((1ull << q) - 1));
         W.c[0][i] = W.c[0][i] - before + (unsigned)k;
         W.s[0][i] = want;
@@ -1998,6 +2010,7 @@ __global__ void __launch_bounds__(256) k_hd_fix(const uint8_t* rec, const HDTabl
 __global__ void k_hd_serial(const uint8_t* rec, const HDTables* T, HDWork W, int fin) {
   if (!T->ok || !W.changed[HD_ROUNDS + 1]) return;
   const unsigned long long nsub = T->nsub;
+  const unsigned long long SB = T->S;
   const uint8_t* pay = rec + T->pay_off;
   for (unsigned long long i = 1; i < nsub; i++) {
     const unsigned long long want = W.e[fin][i - 1];
@@ -2008,23 +2021,30 @@ __global__ void k_hd_serial(const uint8_t* rec, const HDTables* T, HDWork W, int
     if (want == W.s[fin][i]) continue;
     unsigned long long e = want;
     long long c = 0;
-    if (want < (i + 1) * HD_S)
-      c = hd_decode<false>(*T, reinterpret_cast<const HDShared*>(T->lut), pay, want, (i + 1) * HD_S, &e, nullptr);
+    if (want < (i + 1) * SB)
+      c = hd_decode<false>(*T, reinterpret_cast<const HDShared*>(T->lut), pay, want, (i + 1) * SB, &e, nullptr);
     W.s[fin][i] = want;
     W.e[fin][i] = c < 0 ? ~0ull : e;
     W.c[fin][i] = c < 0 ? 0u : (unsigned)c;
   }
 }
 
+// subsequence slots: every stream fits at 512 bits; short ones may use
+// smaller subsequences up to the GPU-filling count
+static unsigned long long hd_nsub_cap(unsigned long long max_payload_bytes) {
+  const unsigned long long at_max = cdiv(max_payload_bytes * 8, (unsigned long long)HD_S_MAX) + 1;
+  return at_max > 4 * HD_FILL ? at_max : 4 * HD_FILL;
+}
+
 size_t huffman_decode_ws_bytes(unsigned long long max_payload_bytes) {
-  const unsigned long long nsub = cdiv(max_payload_bytes * 8, HD_S) + 1;
+  const unsigned long long nsub = hd_nsub_cap(max_payload_bytes);
   return sizeof(HDTables) + 256 + ((HD_ROUNDS + 8) * 4 + 256) + nsub * (8 * 2 + 8 * 2 + 4 * 2 + 8 + 8) + 64;
 }
 
 void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long* len_dev, unsigned long long n,
                                 unsigned long long max_out, unsigned long long max_payload, uint8_t* seq, void* ws,
                                 unsigned long long* lb_ws, DevState* st, cudaStream_t s, int* launches) {
-  const unsigned long long nsub_max = cdiv(max_payload * 8, HD_S) + 1;
+  const unsigned long long nsub_max = hd_nsub_cap(max_payload);
   uint8_t* p = reinterpret_cast<uint8_t*>(ws);
   HDTables* T = reinterpret_cast<HDTables*>(p);
   p += (sizeof(HDTables) + 255) & ~255ull;
@@ -2046,7 +2066,7 @@ void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long*
     W.c[b] = reinterpret_cast<unsigned*>(p);
     p += nsub_max * 4;
   }
-  k_hd_setup<<<1, 256, 0, s>>>(hf_rec, len_dev, n, max_out, T, st);
+  k_hd_setup<<<1, 256, 0, s>>>(hf_rec, len_dev, n, max_out, nsub_max, T, st);
   (*launches)++;
   const unsigned g = persist_grid(cdiv(nsub_max, 256));
   k_hd_first<<<g, 256, 0, s>>>(hf_rec, T, W, st);
