@@ -1265,7 +1265,17 @@ struct HDWork {  // per pass: start, end, count per subsequence
   unsigned long long* off;
   unsigned long long* bmask;  // codeword starts in [i*S, i*S+64) seen by the first pass
   int* changed;               // per pass
+  // streams without a 1-bit code (rough): every codeword start of the first
+  // pass, S bits per subsequence (8 words), so a fix-up syncs anywhere
+  unsigned long long* bmfull;
+  // chain tables (rough streams only): for the subsequences of a window after
+  // each chain head, the decode from every possible start offset d < HD_TD
+  // (end, count); capacity HD_TCAP rows of HD_TD entries
+  unsigned long long* tend;
+  unsigned* tcnt;
 };
+constexpr int HD_TD = 32;                 // start offsets tabulated per subsequence
+constexpr unsigned HD_TCAP = 1u << 16;    // table rows (subsequences) per round
 
 // stages.py:332-368: record checks, Kraft, canonical tables, LUT (parallel)
 __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsigned long long* len_dev,
@@ -1772,6 +1782,55 @@ __device__ long long hd_decode(const HDTables& T, const HDShared* S, const uint8
   return cnt;
 }
 
+// length of the codeword at the reader's position, -1 on an invalid code
+__device__ __forceinline__ int hd_step(const HDTables& T, const HDShared* S, const BitReader& br) {
+  const unsigned key = (unsigned)(br.buf >> (64 - T.K));
+  const uint16_t e = S->lut[key];
+  if (e) return e >> 8;
+  for (int L = T.K + 1; L <= T.maxlen; L++) {
+    if (!T.count[L]) continue;
+    const unsigned long long c = br.peek(L);
+    if (c >= T.first_code[L] && c - T.first_code[L] < (unsigned long long)T.count[L]) return L;
+  }
+  return -1;
+}
+
+// First pass for streams without a 1-bit code: codeword by codeword,
+// recording every codeword start of [s0, stop) (bit q of word q/64).
+__device__ long long hd_first_full(const HDTables& T, const HDShared* S, const uint8_t* pay, unsigned long long s0,
+                                   unsigned long long stop, unsigned long long* endp, unsigned long long* bm) {
+  BitReader br;
+  br.init(pay, T.pay_len, s0);
+  const unsigned long long lim = stop < T.nbits ? stop : T.nbits;
+  unsigned long long pos = s0, word = 0;
+  long long cnt = 0;
+  int cw = 0;
+  bool err = false;
+  while (pos < lim) {
+    const unsigned q = (unsigned)(pos - s0);
+    const int w = (int)(q >> 6);
+    while (cw < w) {
+      bm[cw++] = word;
+      word = 0;
+    }
+    word |= 1ull << (q & 63);
+    const int L = hd_step(T, *&S, br);
+    if (L < 0 || pos + L > T.nbits) {
+      err = true;
+      break;
+    }
+    pos += L;
+    cnt++;
+    br.consume(L);
+  }
+  while (cw < HD_S_MAX / 64) {
+    bm[cw++] = word;
+    word = 0;
+  }
+  *endp = pos;
+  return err ? -1 : cnt;
+}
+
 __global__ void __launch_bounds__(256) k_hd_first(const uint8_t* rec, const HDTables* T, HDWork W, DevState* st) {
   __shared__ HDShared S;
   if (!T->ok) return;
@@ -1784,12 +1843,19 @@ __global__ void __launch_bounds__(256) k_hd_first(const uint8_t* rec, const HDTa
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned long long s0 = i * SB;
     unsigned long long e, m = 0;
-    const long long c = hd_decode<false, true>(*T, &S, pay, s0, s0 + SB, &e, nullptr, &m);
+    long long c;
+    if (T->run_sym >= 0) {
+      c = hd_decode<false, true>(*T, &S, pay, s0, s0 + SB, &e, nullptr, &m);
+    } else {
+      c = hd_first_full(*T, &S, pay, s0, s0 + SB, &e, W.bmfull + i * (HD_S_MAX / 64));
+      m = W.bmfull[i * (HD_S_MAX / 64)];
+    }
     W.bmask[i] = m;
     W.s[0][i] = s0;
     W.e[0][i] = c < 0 ? ~0ull : e;  // error end never matches a successor start
     W.e[1][i] = W.e[0][i];          // first-pass ends, read-only during the fix-up's first round
     W.c[0][i] = c < 0 ? 0u : (unsigned)c;
+    W.s[1][i] = 0;          // no fix-up round has listed it
   }
 }
 
@@ -1907,25 +1973,25 @@ __device__ __forceinline__ void hd_grid_barrier(unsigned* count, volatile unsign
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_hd_fix(const uint8_t* rec, const HDTables* T, HDWork W) {
+// Fix-up round 1 (its own launch: every subsequence independent, full
+// occupancy): each subsequence whose first-pass start disagrees with its
+// predecessor's first-pass end is decoded from that end until it meets one
+// of the first pass's codeword starts (64-bit window), else re-decoded fully.
+__global__ void __launch_bounds__(256, 4) k_hd_fix1(const uint8_t* rec, const HDTables* T, HDWork W) {
   __shared__ HDShared S;
-  __shared__ int s_n;
-  if (!T->ok) return;  // uniform: every block returns
+  if (!T->ok) return;
   hd_load_shared(&S, T);
   __syncthreads();
   const unsigned long long nsub = T->nsub;
   const unsigned long long SB = T->S;
   const uint8_t* pay = rec + T->pay_off;
-  unsigned* bar = reinterpret_cast<unsigned*>(W.changed + HD_ROUNDS + 2);
   volatile unsigned long long* E = W.e[0];
-  // full decode of subsequence i from the predecessor's end
   auto redecode = [&](unsigned long long i, unsigned long long want) {
     unsigned long long e = want;
     long long c = 0;
     if (want < (i + 1) * SB) c = hd_decode<false>(*T, &S, pay, want, (i + 1) * SB, &e, nullptr);
     W.c[0][i] = c < 0 ? 0u : (unsigned)c;
     W.s[0][i] = want;
-    __threadfence();
     E[i] = c < 0 ? ~0ull : e;
   };
   // round 1: every subsequence against the first pass; from the true start
@@ -1940,7 +2006,49 @@ __global__ void __launch_bounds__(256) k_hd_fix(const uint8_t* rec, const HDTabl
     const unsigned long long s0 = W.s[0][i];
     if (want == s0 || want == ~0ull) continue;
     bool done = false;
-    if (E1[i] != ~0ull && want >= i * SB) {
+    if (T->run_sym < 0 && E1[i] != ~0ull && want >= i * SB) {
+      // decode from the true start until a first-pass codeword start anywhere
+      // in the subsequence; reaching the end without one IS the full re-decode
+      const unsigned long long* bw = W.bmfull + i * (HD_S_MAX / 64);
+      const unsigned long long lim = (i + 1) * SB < T->nbits ? (i + 1) * SB : T->nbits;
+      BitReader br;
+      br.init(pay, T->pay_len, want);
+      unsigned long long pos = want, cur = 0;
+      int cw = -1;
+      unsigned k = 0, before = 0;
+      bool synced = false, err = false;
+      while (pos < lim) {
+        const unsigned q = (unsigned)(pos - i * SB);
+        if ((int)(q >> 6) != cw) {  // entering word q/64: count the first pass's starts of the words before it
+          for (int x = cw < 0 ? 0 : cw; x < (int)(q >> 6); x++) before += __popcll(bw[x]);
+          cw = (int)(q >> 6);
+          cur = bw[cw];
+        }
+        if ((cur >> (q & 63)) & 1) {
+          before += __popcll(cur & ((1ull << (q & 63)) - 1));
+          synced = true;
+          break;
+        }
+        const int L = hd_step(*T, &S, br);
+        if (L < 0 || pos + L > T->nbits) {
+          err = true;
+          break;
+        }
+        pos += L;
+        k++;
+        br.consume(L);
+      }
+      if (synced) {
+        W.c[0][i] = W.c[0][i] - before + k;
+        W.s[0][i] = want;
+      } else {
+        W.c[0][i] = err ? 0u : k;
+        W.s[0][i] = want;
+        E[i] = err ? ~0ull : pos;
+      }
+      done = true;
+    }
+    if (!done && E1[i] != ~0ull && want >= i * SB) {
       unsigned long long ps;
       const unsigned long long bm = W.bmask[i];
       const long long k = hd_decode<false, false, true>(*T, &S, pay, want, (i + 1) * SB, &ps, nullptr, nullptr,
@@ -1955,12 +2063,29 @@ __global__ void __launch_bounds__(256) k_hd_fix(const uint8_t* rec, const HDTabl
     }
     if (!done) redecode(i, want);
   }
-  // later rounds: runs of still inconsistent subsequences are chains (the
+}
+
+__global__ void __launch_bounds__(256) k_hd_fix(const uint8_t* rec, const HDTables* T, HDWork W) {
+  __shared__ HDShared S;
+  __shared__ int s_n;
+  if (!T->ok) return;  // uniform: every block returns
+  hd_load_shared(&S, T);
+  __syncthreads();
+  const unsigned long long nsub = T->nsub;
+  const unsigned long long SB = T->S;
+  const uint8_t* pay = rec + T->pay_off;
+  unsigned* bar = reinterpret_cast<unsigned*>(W.changed + HD_ROUNDS + 2);
+  volatile unsigned long long* E = W.e[0];
+  const unsigned long long* E1 = W.e[1];
+  // rounds >= 2: runs of still inconsistent subsequences are chains (the
   // first pass did not resynchronise before their end, e.g. inside periodic
   // stretches); one thread per chain head walks it sequentially until the
   // stored state agrees again or it reaches the next head (its own walker)
   unsigned long long* wl = W.off;     // work list (the scan's offsets are written later)
   unsigned long long* mark = W.s[1];  // round that listed the subsequence
+  const int lane = threadIdx.x & 31;
+  const unsigned long long gwarp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
   for (int r = 2; r <= HD_ROUNDS; r++) {
     hd_grid_barrier(bar, bar + 1, gridDim.x);
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nsub;
@@ -1984,22 +2109,102 @@ __global__ void __launch_bounds__(256) k_hd_fix(const uint8_t* rec, const HDTabl
     __syncthreads();
     const int n = s_n;
     if (n == 0) return;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-      // a chain may alternate: an entry that agrees with its (new)
-      // predecessor can still have moved its own end in round 1, so the walk
-      // goes on while the current or the next entry disagrees
-      auto bad = [&](unsigned long long j) {
-        const unsigned long long want = j == 0 ? 0ull : E[j - 1];
-        return want != ~0ull && want != W.s[0][j];
-      };
-      unsigned long long i = wl[k];
-      for (;;) {
-        if (bad(i))
-          redecode(i, i == 0 ? 0ull : E[i - 1]);
-        else if (i + 1 >= nsub || !bad(i + 1))
-          break;
-        i++;
-        if (i >= nsub || mark[i] == (unsigned long long)r) break;
+    // Chains: the first pass never resynchronised inside them (periodic
+    // stretches of rough streams), so fixing them is sequential.  Every
+    // subsequence of a window of `win` after each head is first decoded from
+    // EVERY start offset d < HD_TD in parallel (the true start of a
+    // subsequence is its predecessor's end, within maxlen bits of its
+    // nominal start); one warp per chain then walks the window with table
+    // lookups -- 8 subsequences per memory round trip -- instead of one
+    // re-decode per subsequence.  A chain longer than the window is picked up
+    // again by the next round's listing.
+    const unsigned win = (unsigned)max(8, min(256, (int)(HD_TCAP / (unsigned)n)) & ~7);  // whole batches of 8
+    const unsigned long long tabn = (unsigned long long)min((unsigned)n, HD_TCAP / win) * win * HD_TD;
+    for (unsigned long long x = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; x < tabn;
+         x += (unsigned long long)gridDim.x * blockDim.x) {
+      const int d = (int)(x % HD_TD);
+      const unsigned long long row = x / HD_TD, k = row / win, jj = wl[k] + row % win;
+      unsigned long long e = ~0ull;
+      unsigned c = 0;
+      if (jj < nsub && d < T->maxlen) {
+        const unsigned long long st0 = jj * SB + d;
+        e = st0;
+        long long cc = 0;
+        if (st0 < (jj + 1) * SB) cc = hd_decode<false>(*T, &S, pay, st0, (jj + 1) * SB, &e, nullptr);
+        if (cc < 0) e = ~0ull;
+        c = cc < 0 ? 0u : (unsigned)cc;
+      }
+      W.tend[x] = e;
+      W.tcnt[x] = c;
+    }
+    hd_grid_barrier(bar, bar + 1, gridDim.x);
+    for (unsigned long long k = gwarp; k < (unsigned long long)n; k += nwarps) {
+      const unsigned long long head = wl[k];
+      const bool tab = k * win * HD_TD < tabn;
+      unsigned long long t = head == 0 ? 0ull : E[head - 1];  // true start of the current subsequence
+      bool stop = t == ~0ull;
+      for (unsigned b0 = 0; !stop && b0 < win; b0 += 8) {
+        // lane l: table entry d = l of the batch's 8 subsequences, and their stored starts / marks
+        unsigned long long te[8], sst = ~0ull, est = ~0ull, mk = 0;
+        unsigned tc[8];
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+          const unsigned long long row = k * win + b0 + b;
+          te[b] = tab ? W.tend[row * HD_TD + lane] : ~0ull;
+          tc[b] = tab ? W.tcnt[row * HD_TD + lane] : 0u;
+        }
+        // lanes 0..8: stored starts of the batch and its successor; 0..7: stored ends, marks
+        if (lane < 9 && head + b0 + lane < nsub) {
+          sst = W.s[0][head + b0 + lane];
+          if (lane < 8) {
+            est = E[head + b0 + lane];
+            mk = mark[head + b0 + lane];
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+          const unsigned long long jj = head + b0 + b;
+          const unsigned long long S_ = __shfl_sync(0xffffffffu, sst, b), S1 = __shfl_sync(0xffffffffu, sst, b + 1),
+                                   E_ = __shfl_sync(0xffffffffu, est, b), M_ = __shfl_sync(0xffffffffu, mk, b);
+          if (stop) continue;
+          if (jj >= nsub || b0 + b >= win || (jj != head && M_ == (unsigned long long)r) || t == ~0ull) {
+            stop = true;  // end of the stream / window, or the next head (its own walker)
+            continue;
+          }
+          unsigned long long e;
+          if (t == S_) {
+            e = E_;  // decoded from its true start already: its end stands
+            if (e == S1) {  // and the successor agrees too: chain resolved
+              stop = true;
+              continue;
+            }
+          } else {
+            const unsigned long long d = t - jj * SB;
+            const int src = d < (unsigned long long)HD_TD ? (int)d : 0;
+            e = __shfl_sync(0xffffffffu, te[b], src);
+            unsigned c = __shfl_sync(0xffffffffu, tc[b], src);
+            if (lane == 0) {
+              if (!tab || t < jj * SB || d >= (unsigned long long)HD_TD || e == ~0ull) {  // not tabulated: decode
+                long long cc = 0;
+                e = t;
+                if (t < (jj + 1) * SB) cc = hd_decode<false>(*T, &S, pay, t, (jj + 1) * SB, &e, nullptr);
+                if (cc < 0) e = ~0ull;
+                c = cc < 0 ? 0u : (unsigned)cc;
+              }
+              // (no fence: only this walker touches the chain; the next
+              // round reads it after a grid barrier)
+              W.c[0][jj] = c;
+              W.s[0][jj] = t;
+              E[jj] = e;
+            }
+            e = __shfl_sync(0xffffffffu, e, 0);
+          }
+          if (jj + 1 >= nsub || e == ~0ull) {
+            stop = true;
+            continue;
+          }
+          t = e;
+        }
       }
     }
   }
@@ -2038,7 +2243,8 @@ static unsigned long long hd_nsub_cap(unsigned long long max_payload_bytes) {
 
 size_t huffman_decode_ws_bytes(unsigned long long max_payload_bytes) {
   const unsigned long long nsub = hd_nsub_cap(max_payload_bytes);
-  return sizeof(HDTables) + 256 + ((HD_ROUNDS + 8) * 4 + 256) + nsub * (8 * 2 + 8 * 2 + 4 * 2 + 8 + 8) + 64;
+  return sizeof(HDTables) + 256 + ((HD_ROUNDS + 8) * 4 + 256) + nsub * (8 * 2 + 8 * 2 + 4 * 2 + 8 + 8) + 64 +
+         (size_t)HD_TCAP * HD_TD * 12 + 64 + nsub * (HD_S_MAX / 8);
 }
 
 void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long* len_dev, unsigned long long n,
@@ -2066,10 +2272,19 @@ void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long*
     W.c[b] = reinterpret_cast<unsigned*>(p);
     p += nsub_max * 4;
   }
+  p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+  W.bmfull = reinterpret_cast<unsigned long long*>(p);
+  p += nsub_max * HD_S_MAX / 8;
+  W.tend = reinterpret_cast<unsigned long long*>(p);
+  p += (size_t)HD_TCAP * HD_TD * 8;
+  W.tcnt = reinterpret_cast<unsigned*>(p);
+  p += (size_t)HD_TCAP * HD_TD * 4;
   k_hd_setup<<<1, 256, 0, s>>>(hf_rec, len_dev, n, max_out, nsub_max, T, st);
   (*launches)++;
   const unsigned g = persist_grid(cdiv(nsub_max, 256));
   k_hd_first<<<g, 256, 0, s>>>(hf_rec, T, W, st);
+  (*launches)++;
+  k_hd_fix1<<<g, 256, 0, s>>>(hf_rec, T, W);
   (*launches)++;
   {  // every block resident (cooperative launch): the fix-up rounds use a grid barrier
     static int per_sm = 0;
@@ -2090,7 +2305,7 @@ void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long*
     cudaLaunchKernelEx(&cfg, k_hd_fix, hf_rec, (const HDTables*)T, W);
     (*launches)++;
     if (getenv("HB_DEBUG_HD")) {
-      std::vector<int> ch(HD_ROUNDS + 4);
+      std::vector<int> ch(HD_ROUNDS + 8);
       cudaStreamSynchronize(s);
       cudaMemcpy(ch.data(), W.changed, ch.size() * 4, cudaMemcpyDeviceToHost);
       int rounds = 1;
