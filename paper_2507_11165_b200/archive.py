@@ -100,12 +100,24 @@ def compress(field: Field, spec: ErrorBoundSpec, mode: str = MODE_CR) -> bytes:
 
 
 def compress_device(field: Field, spec: ErrorBoundSpec, mode: str = MODE_CR, out=None):
-    """Device-resident compress: returns a uint8 CUDA tensor view of the archive."""
+    """Device-resident compress: returns a uint8 CUDA tensor view of the archive.
+
+    Without `out` (or with a smaller one) the archive goes to a buffer of the
+    raw field size + 1 MiB -- the escape rule keeps the stream below the raw
+    code bytes, so only outlier-heavy fields exceed it -- and a call whose
+    archive is longer is re-run into a buffer of the exact length the first
+    call reported (hb_compress_bound's 13 bytes per point are never reserved
+    up front)."""
     import torch
-    cap = compress_bound(field.dims, _prec(field))
-    if out is None or out.numel() < cap:
+    bound = compress_bound(field.dims, _prec(field))
+    cap = out.numel() if out is not None else min(bound, field.count * _prec(field) + (1 << 20))
+    if out is None:
         out = torch.empty(cap, dtype=torch.uint8, device=field.values.device)
-    n = _compress_into(field, spec, mode, out, cap)
+    rc, c, n = _compress_call(field, spec, mode, out, cap)
+    if rc == _lib.HB_EARG and cap < n <= bound:
+        out = torch.empty(n, dtype=torch.uint8, device=field.values.device)
+        rc, c, n = _compress_call(field, spec, mode, out, n)
+    _lib.raise_for(rc, c)
     return out[:n]
 
 
