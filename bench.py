@@ -537,7 +537,6 @@ def run_ours(args):
         e2e = total_bytes / te.item() / 1e9
         line["e2e"] = {"value": round(e2e, 3), "unit": "GB/s", "h2d_bytes_per_step": nbytes + len(blob),
                        "d2h_bytes_per_step": len(blob) + nbytes}
-
     if not args.no_config5:
         _lib.release_contexts()  # the 512^3 arena is not needed for the slabs
         torch.cuda.empty_cache()
