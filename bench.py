@@ -283,7 +283,7 @@ def cpu_baseline(vals_host, args):
                          "sample": f"{s1.shape[0]}x{s1.shape[1]}x{s1.shape[2]} leading slab, 1 round trip"}}
 
 
-C5_DIMS = (2048, 2048, 2048)
+C5_DIMS = (int(os.environ.get("HB_C5_SIZE", "2048")),) * 3  # (a smaller cube only for smoke tests)
 C5_SLABS = 8
 
 
@@ -357,14 +357,16 @@ def config5(args, world, rank, local, stream):
     torch.cuda.synchronize()
     tc = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3
     td = sum(e[1].elapsed_time(e[2]) for e in evs) / 1e3
-    t = torch.tensor([tc + td, tc, td], dtype=torch.float64, device="cuda")
+    t = torch.tensor([tc + td, tc, td], dtype=torch.float64, device="cpu" if dist.is_initialized() and
+                     dist.get_backend() != "nccl" else "cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ttot, tcm, tdm = t.tolist()
     vol = float(np.prod(C5_DIMS)) * 4
     peak, _ = peaks()
-    res = {"workload": "2048^3 f32 turbulence-like (synth.make_modes), 8 axis-0 slabs of 256x2048x2048, "
-                       f"rel-eb {args.eb} (global), {args.mode.upper()}", "scaling": "strong",
+    res = {"workload": f"{C5_DIMS[0]}^3 f32 turbulence-like (synth.make_modes), 8 axis-0 slabs of "
+                       f"{C5_DIMS[0] // 8}x{C5_DIMS[1]}x{C5_DIMS[2]}, rel-eb {args.eb} (global), {args.mode.upper()}",
+           "scaling": "strong",
            "slabs_per_gpu": per, "steps": steps, "warmup": 1,
            "value": round(vol * steps / ttot / 1e9, 3), "unit": "GB/s",
            "compress_gbs": round(vol * steps / tcm / 1e9, 3), "decompress_gbs": round(vol * steps / tdm / 1e9, 3),
@@ -387,9 +389,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HB_BENCH_BACKEND=gloo (and ranks sharing a GPU) only to exercise the N > 1
+    # path on a one-GPU box; the driver's runs use NCCL, one GPU per rank
+    backend = os.environ.get("HB_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    cdev = "cuda" if backend == "nccl" else "cpu"  # collective buffers
     S = args.size
     vals = synth.make_device(args.kind, (S, S, S), seed=2025 + rank)
     f = hb.Field(vals)
@@ -431,7 +441,7 @@ def run_ours(args):
                 # slabs of one volume share the global rel-eb: device min/max
                 # (k_minmax), 2-float all-reduce, then an abs-eb compress
                 lo, hi = field_min_max(f)
-                mm = torch.tensor([float(hi), -float(lo)], dtype=torch.float64, device="cuda")
+                mm = torch.tensor([float(hi), -float(lo)], dtype=torch.float64, device=cdev)
                 dist.all_reduce(mm, op=dist.ReduceOp.MAX)
                 launches += _lib.last_launch_count()
                 eb = slabs.global_abs_eb(spec, np.float32(-mm[1].item()), np.float32(mm[0].item()), np.float32)
@@ -443,9 +453,9 @@ def run_ours(args):
                 phases.setdefault(nm, []).append(ms)
             ev[k][1].record(stream)
             if world > 1:  # slab container: all-gather of archive sizes
-                sz = torch.tensor([a.numel()], dtype=torch.int64, device="cuda")
-                allsz = torch.empty(world, dtype=torch.int64, device="cuda")
-                dist.all_gather_into_tensor(allsz, sz)
+                sz = torch.tensor([a.numel()], dtype=torch.int64, device=cdev)
+                allsz = [torch.empty_like(sz) for _ in range(world)]
+                dist.all_gather(allsz, sz)
             hb.decompress_device(a, f.dims, np.float32, out=rec_buf)
             launches += _lib.last_launch_count()
             for nm, ms in _lib.last_phases():
@@ -468,7 +478,7 @@ def run_ours(args):
     _lib.set_profile(False)
     tc = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3
     td = sum(e[1].elapsed_time(e[2]) for e in ev) / 1e3
-    t = torch.tensor([tc + td, tc, td], dtype=torch.float64, device="cuda")
+    t = torch.tensor([tc + td, tc, td], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ttot, tcm, tdm = t.tolist()
@@ -531,7 +541,7 @@ def run_ours(args):
             blob = hb.compress(fh, spec, args.mode)
             hb.decompress(blob, out=host_out.numpy())
         torch.cuda.synchronize()
-        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=cdev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = total_bytes / te.item() / 1e9
