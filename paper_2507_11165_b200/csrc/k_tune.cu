@@ -218,12 +218,18 @@ __global__ void __launch_bounds__(TUNE_THREADS)
   const bool linear = cb & 1, seq1d = (cb >> 1) & 1;
   const double eb = st->eb, two_eb = st->two_eb, inv_two_eb = __ddiv_rn(1.0, two_eb);
   const int dims[3] = {b0, b1, b2};
-  SubStep ss[7];
-  const int nss = block_steps(dims, level, seq1d, ss);
+  // the level's sub-steps, computed once per CTA into shared memory (a
+  // per-thread table lived in local memory: 688 B of stack per thread that
+  // the 98 KB shared-memory carve-out pushed out of L1)
+  __shared__ SubStep s_ss[7];
+  __shared__ int s_nss;
+  if (threadIdx.x == 0) s_nss = block_steps(dims, level, seq1d, s_ss);
+  __syncthreads();
+  const int nss = s_nss;
   const int s = 1 << (level - 1);
   double total = 0.0;
   for (int t = 0; t < nss; t++) {
-    const SubStep& S = ss[t];
+    const SubStep S = s_ss[t];
     const int n = S.count[0] * S.count[1] * S.count[2];
     const int c12 = S.count[1] * S.count[2];
     const float r2 = 1.0f / (float)S.count[2], r12 = 1.0f / (float)c12;
@@ -234,17 +240,20 @@ __global__ void __launch_bounds__(TUNE_THREADS)
       c[1] = S.start[1] + q1 * S.step[1];
       c[0] = S.start[0] + q0 * S.step[0];
       const int lin = (c[0] * b1 + c[1]) * b2 + c[2];
-      double pv[3];
-      int ov[3];
-      for (int i = 0; i < S.k; i++) {
+      double pv[3] = {0.0, 0.0, 0.0};
+      int ov[3] = {0, 0, 0};
+#pragma unroll
+      for (int i = 0; i < 3; i++) {
+        if (i >= S.k) break;
         const int a = S.axes[i];
+        const int ca = a == 0 ? c[0] : (a == 1 ? c[1] : c[2]), da = a == 0 ? b0 : (a == 1 ? b1 : b2);
         const int stp = (a == 0 ? b1 * b2 : (a == 1 ? b2 : 1)) * s;
-        const int cls = classify(c[a], dims[a], s, linear);
+        const int cls = classify(ca, da, s, linear);
         // samples at -3s, -1s, +1s, +3s; only in-range ones are used by cls
-        const double v0 = c[a] >= 3 * s ? g[lin - 3 * stp] : 0.0;
+        const double v0 = ca >= 3 * s ? g[lin - 3 * stp] : 0.0;
         const double v1 = g[lin - stp];
-        const double v2 = c[a] + s < dims[a] ? g[lin + stp] : 0.0;
-        const double v3 = c[a] + 3 * s < dims[a] ? g[lin + 3 * stp] : 0.0;
+        const double v2 = ca + s < da ? g[lin + stp] : 0.0;
+        const double v3 = ca + 3 * s < da ? g[lin + 3 * stp] : 0.0;
         pv[i] = apply_stencil(cls, v0, v1, v2, v3);
         ov[i] = stencil_order(cls);
       }
