@@ -552,7 +552,7 @@ __device__ __forceinline__ bool tp_block(const TPassArgs& A, const TMaps& M, int
 // by the other classes.
 template <typename T, bool DEC, int K, bool LINEAR, bool LV1, int C0 = -1, int C1 = -1, int C2 = -1,
           int TX = txof(K)>
-__global__ void __launch_bounds__(T_THREADS, C0 >= 0 ? 4 : 2) k_tpass(const __grid_constant__ TPassArgs A,
+__global__ void __launch_bounds__(T_THREADS, C0 >= 0 ? (C1 >= 0 && !DEC ? 3 : 4) : 2) k_tpass(const __grid_constant__ TPassArgs A,
                                                          const __grid_constant__ TMaps M) {
   extern __shared__ __align__(128) double tiles[];
   __shared__ unsigned shist[256];

@@ -1871,7 +1871,7 @@ __global__ void __launch_bounds__(256) k_hd_scan(const HDTables* T, HDWork W, in
   if (!T->ok) return;
   const unsigned long long nsub = T->nsub;
   const unsigned long long ntiles = cdiv(nsub, (unsigned long long)HS_TILE);
-  const unsigned* c = W.c[fin];
+  const unsigned* c = (fin ? W.c[1] : W.c[0]);
   for (;;) {
     if (threadIdx.x == 0) tile_sh = atomicAdd(lb, 1ull);
     __syncthreads();
@@ -1906,7 +1906,7 @@ __global__ void __launch_bounds__(256) k_hd_scan(const HDTables* T, HDWork W, in
     if (tile == ntiles - 1 && threadIdx.x == 0) {
       const unsigned long long tot = base_sh + total;
       if (tot != T->nsym) raise_flag(st, F_STAGE, 160);
-      if (W.e[fin][nsub - 1] != T->nbits) raise_flag(st, F_STAGE, 161);
+      if ((fin ? W.e[1] : W.e[0])[nsub - 1] != T->nbits) raise_flag(st, F_STAGE, 161);
     }
     __syncthreads();
   }
@@ -1926,9 +1926,9 @@ __global__ void __launch_bounds__(256, 4) k_hd_emit(const uint8_t* rec, const HD
   bool bad = false;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nsub;
        i += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long s0 = W.s[fin][i];
-    const unsigned long long want = i == 0 ? 0ull : W.e[fin][i - 1];
-    if (want != s0 || W.e[fin][i] == ~0ull) {
+    const unsigned long long s0 = (fin ? W.s[1] : W.s[0])[i];
+    const unsigned long long want = i == 0 ? 0ull : (fin ? W.e[1] : W.e[0])[i - 1];
+    if (want != s0 || (fin ? W.e[1] : W.e[0])[i] == ~0ull) {
       bad = true;
       continue;
     }
@@ -2218,19 +2218,19 @@ __global__ void k_hd_serial(const uint8_t* rec, const HDTables* T, HDWork W, int
   const unsigned long long SB = T->S;
   const uint8_t* pay = rec + T->pay_off;
   for (unsigned long long i = 1; i < nsub; i++) {
-    const unsigned long long want = W.e[fin][i - 1];
+    const unsigned long long want = (fin ? W.e[1] : W.e[0])[i - 1];
     if (want == ~0ull) {
-      W.e[fin][i] = ~0ull;
+      (fin ? W.e[1] : W.e[0])[i] = ~0ull;
       continue;
     }
-    if (want == W.s[fin][i]) continue;
+    if (want == (fin ? W.s[1] : W.s[0])[i]) continue;
     unsigned long long e = want;
     long long c = 0;
     if (want < (i + 1) * SB)
       c = hd_decode<false>(*T, reinterpret_cast<const HDShared*>(T->lut), pay, want, (i + 1) * SB, &e, nullptr);
-    W.s[fin][i] = want;
-    W.e[fin][i] = c < 0 ? ~0ull : e;
-    W.c[fin][i] = c < 0 ? 0u : (unsigned)c;
+    (fin ? W.s[1] : W.s[0])[i] = want;
+    (fin ? W.e[1] : W.e[0])[i] = c < 0 ? ~0ull : e;
+    (fin ? W.c[1] : W.c[0])[i] = c < 0 ? 0u : (unsigned)c;
   }
 }
 
