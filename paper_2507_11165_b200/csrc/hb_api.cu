@@ -1000,9 +1000,12 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
   // length on the device: one synchronisation per call instead of two
   bool dev_out = false;
   if (!tune_only) {
+    // a failed launch must not be cleared with the pointer query's own error
+    CU(cudaGetLastError());
     cudaPointerAttributes pa;
-    dev_out = cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
-    cudaGetLastError();
+    const cudaError_t pe = cudaPointerGetAttributes(&pa, out);
+    dev_out = pe == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+    if (pe != cudaSuccess) cudaGetLastError();
     if (dev_out) launch_archive_copy(static_cast<uint8_t*>(out), arch, st, cap, s, &nl);
   }
   ctx->launches = nl;

@@ -474,15 +474,15 @@ template <typename T, bool DEC, int CFG, int OID>
 static int col_launch_one(const LvArgs& A, unsigned /*blocks*/, cudaStream_t s) {
   using TL = Tile3;
   constexpr size_t smem = (size_t)Lay<TL, (CFG & 2) == 0>::total() * 8;
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [&] {  // once per process, thread-safe (C++11 static init)
     for (const void* f : {(const void*)k_level_col<TL, T, DEC, CFG, OID, true>,
                           (const void*)k_level_col<TL, T, DEC, CFG, OID, false>}) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   // interior box per axis: tiles t with 16t >= 2 and 16t + 16 + 3 <= D
   ColPart P;
   bool empty = false;

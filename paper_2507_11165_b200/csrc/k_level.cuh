@@ -411,16 +411,16 @@ static inline bool launch_tiled(LevelGeom g, const LvArgs& base, int prec, cudaS
   A.g = g;
   const unsigned blocks = (unsigned)((long long)g.ntile[0] * g.ntile[1] * g.ntile[2]);
   const int oid = order_id(g);
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [&] {  // once per process, thread-safe (C++11 static init)
     auto set = [](const void* f, int bytes) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     };
     set((const void*)k_level_tiled<Tile2, float, DEC>, Tile2::smem_bytes());
     set((const void*)k_level_tiled<Tile2, double, DEC>, Tile2::smem_bytes());
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   {
     const size_t smem = Tile2::smem_bytes();
     if (prec == 4)

@@ -861,16 +861,16 @@ __global__ void __launch_bounds__(MT, 2) k_march(const __grid_constant__ MarchAr
 constexpr int MTY = 32, MTZ = 32;
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  // thread-safe one-time lookup (a 'tried' flag set before the pointer let a
+  // concurrent caller see no entry point and take another kernel path)
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult qr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
         qr == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+  }();
   return fn;
 }
 
@@ -891,12 +891,12 @@ bool encode3(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esz, 
 template <typename T, bool DEC, bool LINEAR, bool LV1>
 void launch_march(const MarchArgs& A, cudaStream_t s) {
   using G = MG<MTY, MTZ, DEC ? 0 : sizeof(T)>;
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [&] {  // once per process, thread-safe (C++11 static init)
     cudaFuncSetAttribute((const void*)k_march<T, DEC, LINEAR, LV1, MTY, MTZ>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::bytes);
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   const LevelGeom& g = A.g;
   const dim3 grid((unsigned)((g.D[2] + MTZ - 1) / MTZ), (unsigned)((g.D[1] + MTY - 1) / MTY),
                   (unsigned)((A.nep + A.seg - 1) / A.seg));

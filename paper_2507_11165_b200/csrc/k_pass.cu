@@ -742,16 +742,16 @@ __global__ void k_gather0(const double* __restrict__ E, LevelGeom g, double* __r
 
 // ------------------------------------------------------------------ host
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  // thread-safe one-time lookup (a 'tried' flag set before the pointer let a
+  // concurrent caller see no entry point and take another kernel path)
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+  }();
   return fn;
 }
 
@@ -875,12 +875,12 @@ void launch_step(const Launch& L, cudaStream_t s, int* launches) {
     my = std::max(my, (n1 + TY - 1) / TY);
   }
   const size_t smem = (size_t)K * slot_of(txof(K)) * 8;
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [&] {  // once per process, thread-safe (C++11 static init)
     cudaFuncSetAttribute((const void*)k_tpass<T, DEC, K, LINEAR, LV1, C0, C1, C2>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   const dim3 grid((unsigned)mz, (unsigned)my, (unsigned)(A.nbx * A.ncls));
   k_tpass<T, DEC, K, LINEAR, LV1, C0, C1, C2><<<grid, T_THREADS, smem, s>>>(A, L.M);
   (*launches)++;
@@ -930,13 +930,13 @@ bool launch_sweep(const Launch& base, cudaStream_t s, int* launches) {
   S.done = S.ticket + 1;
   cudaMemsetAsync(S.ticket, 0, sizeof(unsigned) * (1 + 3 * (size_t)S.nslab), s);
   const size_t smem = (size_t)3 * slot_of(4) * 8;
-  static int per_sm = 0;
-  if (!per_sm) {
+  static const int per_sm = [&] {
     cudaFuncSetAttribute((const void*)k_tsweep<T, DEC, LINEAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tsweep<T, DEC, LINEAR>, T_THREADS, smem);
-    if (per_sm < 1) per_sm = 1;
-  }
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_tsweep<T, DEC, LINEAR>, T_THREADS, smem);
+    return v < 1 ? 1 : v;
+  }();
   S.one = sweep_mode() == 1;
   const int grid = S.one ? S.nitems : std::min(S.nitems, kSMs * per_sm);
   k_tsweep<T, DEC, LINEAR><<<grid, T_THREADS, smem, s>>>(S, SM);

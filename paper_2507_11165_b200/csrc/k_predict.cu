@@ -531,14 +531,15 @@ __global__ void __launch_bounds__(256) k_level(LevelGeom g, const T* __restrict_
   }
 }
 
-static bool g_smem_init = false;
 void level_kernel_smem_init() {
-  if (g_smem_init) return;
-  cudaFuncSetAttribute(k_level<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_level<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_level<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_level<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  g_smem_init = true;
+  static const bool done = [] {  // once per process, thread-safe
+    cudaFuncSetAttribute(k_level<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_level<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_level<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_level<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return true;
+  }();
+  (void)done;
 }
 
 void launch_level_compress(const LevelGeom& g, const void* field, int prec, double* E, uint8_t* seq, uint32_t* obm,

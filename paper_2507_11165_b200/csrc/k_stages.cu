@@ -476,12 +476,12 @@ void launch_reduce_chain_impl(int stage, int width, int src_kind, const uint8_t*
   switch (src_kind) {
     case SRC_MEM:
       if (width <= 4) {
-        static bool attr = false;
-        if (!attr) {
+        static const bool attr = [&] {  // once per process, thread-safe (C++11 static init)
           cudaFuncSetAttribute(k_reduce0<MemSrc, uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                RD_TILE * 4);
-          attr = true;
-        }
+          return true;
+        }();
+        (void)attr;
         k_reduce0<MemSrc, uint32_t><<<g0, RD_THREADS, stg, s>>>(MemSrc{src_ptr, 0, width}, len_dev, stage, width,
                                                                 bm, bufs.bitmap[0], bufs.payload[0], lb_ws);
       } else {
@@ -829,11 +829,11 @@ void launch_huffman_encode(const uint8_t* seq, unsigned long long n, uint8_t* hf
   k_huff_zero<<<PERSIST_CTAS, 256, 0, s>>>(reinterpret_cast<uint32_t*>(hf_rec), st);
   (*launches)++;
   if (n == 0) return;
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [&] {  // once per process, thread-safe (C++11 static init)
     cudaFuncSetAttribute(k_huff_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, HE_SMEM_WORDS * 4);
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   const unsigned long long tiles = cdiv(n, HE_TILE);
   k_huff_encode<<<persist_grid(tiles), 256, HE_SMEM_WORDS * 4, s>>>(seq, n, reinterpret_cast<uint32_t*>(hf_rec),
                                                                    lb_ws, st);
@@ -2287,11 +2287,11 @@ void launch_huffman_decode_impl(const uint8_t* hf_rec, const unsigned long long*
   k_hd_fix1<<<g, 256, 0, s>>>(hf_rec, T, W);
   (*launches)++;
   {  // every block resident (cooperative launch): the fix-up rounds use a grid barrier
-    static int per_sm = 0;
-    if (!per_sm) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hd_fix, 256, 0);
-      if (per_sm < 1) per_sm = 1;
-    }
+    static const int per_sm = [] {
+      int v = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_hd_fix, 256, 0);
+      return v < 1 ? 1 : v;
+    }();
     const unsigned gf = (unsigned)std::min<unsigned long long>(cdiv(nsub_max, 256), (unsigned long long)kSMs * per_sm);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(gf);

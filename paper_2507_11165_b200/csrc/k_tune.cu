@@ -341,14 +341,21 @@ void launch_tune_level(const TunePlan& p, const void* field, int prec, const uin
   double* borig = trials + (size_t)2 * 4 * p.nb * p.bn;
   unsigned* done = reinterpret_cast<unsigned*>(borig + (size_t)p.nb * p.bn);
   if (level == p.top) cudaMemsetAsync(done, 0, sizeof(unsigned), s);
+  // the attribute is process-wide: set once to the largest plan tune_supported
+  // admits (a per-launch value raced between threads compressing different
+  // shapes, failing the other thread's launch)
+  static const bool attr = [] {
+    cudaFuncSetAttribute(k_tune_level<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tune_level<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return true;
+  }();
+  (void)attr;
   if (prec == 4) {
-    cudaFuncSetAttribute(k_tune_level<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_tune_level<float><<<4 * p.nb, TUNE_THREADS, smem, s>>>((const float*)field, dims[1], dims[2], origins, p.nb,
                                                              p.shape[0], p.shape[1], p.shape[2], p.top, level, trials,
                                                              berr, st, reinterpret_cast<float*>(borig), done,
                                                              host_cfg);
   } else {
-    cudaFuncSetAttribute(k_tune_level<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_tune_level<double><<<4 * p.nb, TUNE_THREADS, smem, s>>>((const double*)field, dims[1], dims[2], origins, p.nb,
                                                               p.shape[0], p.shape[1], p.shape[2], p.top, level,
                                                               trials, berr, st, borig, done, host_cfg);
