@@ -416,6 +416,10 @@ def run_ours(args):
         hb.decompress_device(a, f.dims, np.float32, out=rec_buf)
         return a
 
+    # the timed region's profiling mode (only the level-pass marks, the
+    # dominant kernel's CUDA events for the roofline) is on for the warm-up
+    # too: the compress graph is captured on the third identical call
+    _lib.set_profile(2)
     for _ in range(args.warmup):
         arch = step()
     # correctness guard on the timed configuration
@@ -427,7 +431,6 @@ def run_ours(args):
     # timed region: only the level-pass marks (the dominant kernel's CUDA
     # events for the roofline); the full phase table comes from an untimed
     # profiled pass afterwards
-    _lib.set_profile(2)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     phases = {}
     launches = 0

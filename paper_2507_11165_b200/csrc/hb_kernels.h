@@ -106,7 +106,8 @@ bool tune_supported(const TunePlan& p);
 size_t tune_ws_bytes(const TunePlan& p);
 void launch_tune_level(const TunePlan& p, const void* field, int prec, const uint64_t dims[3],
                        const unsigned long long* origins, int level, double* trials, double* berr, DevState* st,
-                       cudaStream_t s, int* launches, uint8_t* host_cfg = nullptr);
+                       cudaStream_t s, int* launches, uint8_t* host_cfg = nullptr,
+                       cudaGraphConditionalHandle cond = 0);
 // whole-field blocks too large for shared memory
 size_t tune_global_bytes(unsigned long long bn);
 int launch_tune_global(const void* field, int prec, const uint64_t dims[3], int top, uint8_t* scratch,

@@ -141,7 +141,8 @@ __device__ __forceinline__ int qdiv(int a, int b, float rb) {
 // tuning.py:135-140 for one level, run by the first warp of the CTA that
 // finishes the level last (k_tune_level): Neumaier sum of the block errors per
 // config, (err, index) argmin, winner handed to the next level.
-__device__ void tune_select(int nb, int level, const double* berr, DevState* st, uint8_t* host_cfg) {
+__device__ void tune_select(int nb, int level, const double* berr, DevState* st, uint8_t* host_cfg,
+                            cudaGraphConditionalHandle cond) {
   __shared__ double e[4];
   const int ci = threadIdx.x;
   if (ci < 4) {
@@ -168,6 +169,9 @@ __device__ void tune_select(int nb, int level, const double* berr, DevState* st,
     st->tune_winner[level - 1] = best;
     st->cfg[level - 1] = c_choice[best];
     __threadfence();
+    // inside the compress graph: the level's switch node runs body `best`
+    // (the level passes of that config) -- no host round trip
+    if (cond) cudaGraphSetConditional(cond, (unsigned)best);
     if (host_cfg) {  // mapped pinned memory: the host reads it once an event after this kernel completes
       host_cfg[level - 1] = c_choice[best];
       __threadfence_system();
@@ -179,7 +183,7 @@ template <typename T>
 __global__ void __launch_bounds__(TUNE_THREADS)
     k_tune_level(const T* __restrict__ field, long long fd1, long long fd2, const unsigned long long* origins, int nb,
                  int b0, int b1, int b2, int top, int level, double* trials, double* berr, DevState* st,
-                 T* borig, unsigned* done, uint8_t* host_cfg) {
+                 T* borig, unsigned* done, uint8_t* host_cfg, cudaGraphConditionalHandle cond) {
   extern __shared__ double tsm[];
   const int bn = b0 * b1 * b2;
   double* g = tsm;
@@ -319,7 +323,7 @@ __global__ void __launch_bounds__(TUNE_THREADS)
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x < 32) tune_select(nb, level, berr, st, host_cfg);
+  if (threadIdx.x < 32) tune_select(nb, level, berr, st, host_cfg, cond);
   if (threadIdx.x == 0) *done = 0;  // ready for the next level / call
 }
 
@@ -336,7 +340,7 @@ size_t tune_ws_bytes(const TunePlan& p) {
 
 void launch_tune_level(const TunePlan& p, const void* field, int prec, const uint64_t dims[3],
                        const unsigned long long* origins, int level, double* trials, double* berr, DevState* st,
-                       cudaStream_t s, int* launches, uint8_t* host_cfg) {
+                       cudaStream_t s, int* launches, uint8_t* host_cfg, cudaGraphConditionalHandle cond) {
   const size_t smem = tune_smem(p, prec);
   double* borig = trials + (size_t)2 * 4 * p.nb * p.bn;
   unsigned* done = reinterpret_cast<unsigned*>(borig + (size_t)p.nb * p.bn);
@@ -354,11 +358,11 @@ void launch_tune_level(const TunePlan& p, const void* field, int prec, const uin
     k_tune_level<float><<<4 * p.nb, TUNE_THREADS, smem, s>>>((const float*)field, dims[1], dims[2], origins, p.nb,
                                                              p.shape[0], p.shape[1], p.shape[2], p.top, level, trials,
                                                              berr, st, reinterpret_cast<float*>(borig), done,
-                                                             host_cfg);
+                                                             host_cfg, cond);
   } else {
     k_tune_level<double><<<4 * p.nb, TUNE_THREADS, smem, s>>>((const double*)field, dims[1], dims[2], origins, p.nb,
                                                               p.shape[0], p.shape[1], p.shape[2], p.top, level,
-                                                              trials, berr, st, borig, done, host_cfg);
+                                                              trials, berr, st, borig, done, host_cfg, cond);
   }
   (*launches)++;
 }

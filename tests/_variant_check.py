@@ -42,7 +42,7 @@ def main() -> int:
         for mode in ("cr", "tp"):
             ref = oracle.compress(vals, "rel", mag, mode, len(dims))
             back, _ = oracle.decompress(ref)
-            for rep in range(2):  # second call: graph replays where enabled
+            for rep in range(4):  # later calls: graph capture / replays where enabled
                 arch = hb.compress_device(f_dev, spec, mode)
                 if arch.cpu().numpy().tobytes() != ref:
                     print(f"archive mismatch {kind} {dims} {dt} {mode} rep {rep}")

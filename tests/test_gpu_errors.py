@@ -162,6 +162,7 @@ def test_concurrent_compress_threads(oracle):
               (("grf", (40, 50, 60), 1), ("rough", (33, 48, 21), 2), ("gauss", (64, 64, 64), 3),
                ("grf", (300, 400), 4))]
     refs = [oracle.compress(v, "rel", 1e-3, "cr", v.ndim) for v in fields]
+    backs = [oracle.decompress(r)[0] for r in refs]
     spec = hb.ErrorBoundSpec("rel", 1e-3)
     errors = []
 
@@ -171,6 +172,9 @@ def test_concurrent_compress_threads(oracle):
                 blob = hb.compress(hb.Field(fields[i], ndim=fields[i].ndim), spec, "cr")
                 if blob != refs[i]:
                     errors.append(i)
+                out = hb.decompress(refs[i])  # decompress is reentrant too
+                if not np.array_equal(out.values.reshape(-1), backs[i].reshape(-1)):
+                    errors.append(f"decompress {i}")
             hb._lib.release_contexts()
         except Exception as e:  # pragma: no cover - reported below
             errors.append(repr(e))

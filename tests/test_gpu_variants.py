@@ -7,6 +7,7 @@ others so none of them ships untested:
   HB_TILED_LEVELS    column-mapped 3D tile kernel (k_col.cuh) instead of TMA passes
   HB_GENERIC_LEVELS  generic per-phase kernel (k_predict.cu) for every level
   HB_NO_GRAPHS       no CUDA-graph capture/replay of the compress tail / decompress
+  HB_NO_FULL_GRAPH   host-driven tuner/level overlap instead of the conditional-node compress graph
   HB_SERIAL_TUNE     tuner and level passes on one stream (no overlap)
   HB_MARCH=1         axis-0 marching level kernel (k_march.cu) for multidim 3D levels
   HB_SWEEP=2 / 1     level 1 as one slab-ordered sweep (persistent / one item per CTA)
@@ -29,6 +30,7 @@ VARIANTS = {
     "tiled": {"HB_TILED_LEVELS": "1"},
     "generic": {"HB_GENERIC_LEVELS": "1"},
     "no-graphs": {"HB_NO_GRAPHS": "1"},
+    "no-full-graph": {"HB_NO_FULL_GRAPH": "1"},
     "serial-tune": {"HB_SERIAL_TUNE": "1"},
     "march": {"HB_MARCH": "1"},
     "sweep": {"HB_SWEEP": "2"},
