@@ -221,9 +221,14 @@ struct TpSrc {
 // WT: register word type (32-bit for widths <= 4: half the registers).
 // stg: shared staging for the tile's kept words (widths <= 4), written out
 // with coalesced stores once the tile's base is known; null = direct stores.
-template <class Src, typename WT>
-__device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage, int width, uint8_t* bitmap,
+// ST / W: compile-time stage / width (0 = take the runtime argument); the
+// chains the compressor runs are instantiated with both fixed, so each kernel
+// holds only its own width's load/store code.
+template <class Src, typename WT, int ST = 0, int W = 0>
+__device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage_rt, int width_rt, uint8_t* bitmap,
                              uint8_t* payload, unsigned long long* lb, BmLevel* lv, uint8_t* stg) {
+  const int stage = ST ? ST : stage_rt;
+  const int width = W ? W : width_rt;
   __shared__ unsigned long long sh[33];
   __shared__ unsigned long long tile_sh, base_sh;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -317,18 +322,22 @@ __device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage, i
 }
 
 // level 0 of a chain over a typed source
-template <class Src, typename WT>
+template <class Src, typename WT, int ST = 0, int W = 0>
 __global__ void __launch_bounds__(RD_THREADS, sizeof(WT) == 4 ? 4 : 1)
-    k_reduce0(Src src, const unsigned long long* len_dev, int stage, int width, BmState* bm, uint8_t* bitmap,
+    k_reduce0(Src src, const unsigned long long* len_dev, int stage_rt, int width_rt, BmState* bm, uint8_t* bitmap,
               uint8_t* payload, unsigned long long* lb) {
   extern __shared__ __align__(16) uint8_t rd_stg[];
+  const int stage = ST ? ST : stage_rt;
+  const int width = W ? W : width_rt;
   Src s2 = src;
   unsigned long long len;
   if constexpr (sizeof(Src) == sizeof(MemSrc) && __is_same(Src, MemSrc)) {
     len = *len_dev;
     s2.len = len;
+    if constexpr (W != 0) s2.w = W;
   } else if constexpr (__is_same(Src, TcmsSrc)) {
     s2.n = *len_dev;
+    if constexpr (W != 0) s2.tw = 8;  // the CR chain's TCMS8 record
     len = s2.len();
   } else {
     s2.n = *len_dev;
@@ -342,7 +351,7 @@ __global__ void __launch_bounds__(RD_THREADS, sizeof(WT) == 4 ? 4 : 1)
     lv->bm_len = cdiv(nw, 8);
     lv->active = 1;
   }
-  reduce_tiles<Src, WT>(s2, nw, stage, width, bitmap, payload, lb, lv, width <= 4 ? rd_stg : nullptr);
+  reduce_tiles<Src, WT, ST, W>(s2, nw, stage, width, bitmap, payload, lb, lv, width <= 4 ? rd_stg : nullptr);
 }
 
 // nested RRE1 over the previous level's bitmap (stages.py:178-181)
@@ -361,7 +370,7 @@ __global__ void __launch_bounds__(RD_THREADS, 4)
     lv->bm_len = cdiv(nw, 8);
     lv->active = 1;
   }
-  reduce_tiles<MemSrc, uint32_t>(src, nw, 2, 1, bitmap, payload, lb, lv, stg);
+  reduce_tiles<MemSrc, uint32_t, 2, 1>(src, nw, 2, 1, bitmap, payload, lb, lv, stg);
 }
 
 // dst[0..n) = src[0..n) for a 4-byte aligned src and any dst: aligned 32-bit
@@ -475,8 +484,18 @@ void launch_reduce_chain_impl(int stage, int width, int src_kind, const uint8_t*
   const size_t stg = width <= 4 ? (size_t)RD_TILE * width : 0;
   switch (src_kind) {
     case SRC_MEM:
-      if (width <= 4) {
+      if (stage == 2 && width == 4) {  // CR: RRE4 over the Huffman record
         static const bool attr = [&] {  // once per process, thread-safe (C++11 static init)
+          cudaFuncSetAttribute(k_reduce0<MemSrc, uint32_t, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               RD_TILE * 4);
+          return true;
+        }();
+        (void)attr;
+        k_reduce0<MemSrc, uint32_t, 2, 4><<<g0, RD_THREADS, stg, s>>>(MemSrc{src_ptr, 0, width}, len_dev, stage,
+                                                                      width, bm, bufs.bitmap[0], bufs.payload[0],
+                                                                      lb_ws);
+      } else if (width <= 4) {
+        static const bool attr = [&] {
           cudaFuncSetAttribute(k_reduce0<MemSrc, uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                RD_TILE * 4);
           return true;
@@ -490,12 +509,17 @@ void launch_reduce_chain_impl(int stage, int width, int src_kind, const uint8_t*
       }
       break;
     case SRC_TCMS:
-      k_reduce0<TcmsSrc, uint32_t><<<g0, RD_THREADS, stg, s>>>(TcmsSrc{src_ptr, 0, tw}, len_dev, stage, width, bm,
-                                                               bufs.bitmap[0], bufs.payload[0], lb_ws);
+      if (stage == 3 && width == 1 && tw == 8)  // CR: RZE1 over TCMS8
+        k_reduce0<TcmsSrc, uint32_t, 3, 1><<<g0, RD_THREADS, stg, s>>>(TcmsSrc{src_ptr, 0, tw}, len_dev, stage,
+                                                                       width, bm, bufs.bitmap[0], bufs.payload[0],
+                                                                       lb_ws);
+      else
+        k_reduce0<TcmsSrc, uint32_t><<<g0, RD_THREADS, stg, s>>>(TcmsSrc{src_ptr, 0, tw}, len_dev, stage, width,
+                                                                 bm, bufs.bitmap[0], bufs.payload[0], lb_ws);
       break;
-    default:
-      k_reduce0<TpSrc, uint32_t><<<g0, RD_THREADS, stg, s>>>(TpSrc{src_ptr, 0}, len_dev, stage, width, bm,
-                                                             bufs.bitmap[0], bufs.payload[0], lb_ws);
+    default:  // TP: RRE1 over BIT1(TCMS1)
+      k_reduce0<TpSrc, uint32_t, 2, 1><<<g0, RD_THREADS, stg, s>>>(TpSrc{src_ptr, 0}, len_dev, stage, width, bm,
+                                                                   bufs.bitmap[0], bufs.payload[0], lb_ws);
       break;
   }
   (*launches)++;
@@ -938,25 +962,19 @@ __global__ void k_bm_parse(int stage, const uint8_t* rec, const unsigned long lo
   D->ok = 1;
 }
 
-// decode one level: bitmap bits + payload -> words (RRE: kept[cumsum-1], RZE: scatter)
-__global__ void __launch_bounds__(RD_THREADS)
-    k_bm_decode(int stage, int k, const uint8_t* rec, const BmDec* D, const uint8_t* inner_bitmap, uint8_t* out,
-                unsigned long long* lb, DevState* st) {
+// decode one level: bitmap bits + payload -> words (RRE: kept[cumsum-1], RZE: scatter).
+// STG / W: compile-time stage / width of the level (0 = runtime), one body
+// per combination the archives hold so each runs only its own width's code.
+template <int STG, int W>
+__device__ __forceinline__ void bm_decode_level(int stg_rt, int w_rt, unsigned long long nsym, const uint8_t* bm,
+                                                const uint8_t* pay, unsigned long long npay, uint8_t* out,
+                                                unsigned long long* lb, DevState* st) {
   __shared__ unsigned long long sh[33];
   __shared__ unsigned long long tile_sh, base_sh;
-  if (!D->ok || k > D->last) return;
-  const int w = D->w[k];
-  const int stg = k == 0 ? stage : 2;
-  const unsigned long long nsym = D->nsym[k];
-  const uint8_t* bm = k == D->last ? rec + D->bm_off[k] : inner_bitmap;
-  const uint8_t* pay = rec + D->pay_off[k];
-  const unsigned long long npay = D->pay_len[k] / w;
+  const int stg = STG ? STG : stg_rt;
+  const int w = W ? W : w_rt;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned long long ntiles = cdiv(nsym, RD_TILE);
-  if (nsym == 0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0 && npay != 0) raise_flag(st, F_STAGE, 120);
-    return;
-  }
   for (;;) {
     if (threadIdx.x == 0) tile_sh = atomicAdd(lb, 1ull);
     __syncthreads();
@@ -1027,6 +1045,30 @@ __global__ void __launch_bounds__(RD_THREADS)
     if (tile == ntiles - 1 && threadIdx.x == 0 && base_sh + total != npay) raise_flag(st, F_STAGE, 122);
     __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(RD_THREADS)
+    k_bm_decode(int stage, int k, const uint8_t* rec, const BmDec* D, const uint8_t* inner_bitmap, uint8_t* out,
+                unsigned long long* lb, DevState* st) {
+  if (!D->ok || k > D->last) return;
+  const int w = D->w[k];
+  const int stg = k == 0 ? stage : 2;
+  const unsigned long long nsym = D->nsym[k];
+  const uint8_t* bm = k == D->last ? rec + D->bm_off[k] : inner_bitmap;
+  const uint8_t* pay = rec + D->pay_off[k];
+  const unsigned long long npay = D->pay_len[k] / w;
+  if (nsym == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && npay != 0) raise_flag(st, F_STAGE, 120);
+    return;
+  }
+  if (stg == 2 && w == 1)  // TP RRE1 and every nested level
+    bm_decode_level<2, 1>(stg, w, nsym, bm, pay, npay, out, lb, st);
+  else if (stg == 2 && w == 4)  // CR RRE4
+    bm_decode_level<2, 4>(stg, w, nsym, bm, pay, npay, out, lb, st);
+  else if (stg == 3 && w == 1)  // CR RZE1
+    bm_decode_level<3, 1>(stg, w, nsym, bm, pay, npay, out, lb, st);
+  else
+    bm_decode_level<0, 0>(stg, w, nsym, bm, pay, npay, out, lb, st);
 }
 
 void launch_reduce_decode_impl(int stage, const uint8_t* rec, const unsigned long long* rec_len_dev,
