@@ -1117,14 +1117,23 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
     ctx->mark("tune");
     static const char* lvl_names[5] = {"", "level1", "level2", "level3", "level4"};
     uint8_t hcfg[4] = {0, 0, 0, 0};
+    // a field with a unit axis (2D) has no level kernel instantiated per
+    // config (those need three non-degenerate axes): its kernels read the
+    // tuned config on the device, so the level passes just wait on the
+    // tuner's event -- no host round trip per level
+    const bool dev_cfg = dims[0] == 1 || dims[1] == 1 || dims[2] == 1;
     for (int level = top; level >= 1; level--) {
-      CU(cudaEventSynchronize(ctx->ev_tune[level]));
-      hcfg[level - 1] = reinterpret_cast<volatile uint8_t*>(pc)[level - 1];
+      if (dev_cfg) {
+        CU(cudaStreamWaitEvent(s2, ctx->ev_tune[level], 0));
+      } else {
+        CU(cudaEventSynchronize(ctx->ev_tune[level]));
+        hcfg[level - 1] = reinterpret_cast<volatile uint8_t*>(pc)[level - 1];
+      }
       LevelGeom g;
       make_level_geom(dims, level, &g);
       const bool rng = level == 1 && ncu_range("level1");
       if (rng) cudaProfilerStart();
-      launch_level_compress(g, dfield, prec, E, seq, obm, st, s2, &nl, hcfg[level - 1] & 3,
+      launch_level_compress(g, dfield, prec, E, seq, obm, st, s2, &nl, dev_cfg ? -1 : hcfg[level - 1] & 3,
                             reinterpret_cast<double*>(base + o_scr));
       if (rng) cudaProfilerStop();
       ctx->mark_on(lvl_names[level], s2);

@@ -34,6 +34,7 @@ struct BmLevel {
   unsigned long long rec_len; // encoded record length (after nesting decision)
   int flag;                   // bitmap section is a nested record
   int active;                 // level was computed
+  unsigned long long tiles_done;  // k_reduce_tail: completed tiles of this level
 };
 
 struct BmState {

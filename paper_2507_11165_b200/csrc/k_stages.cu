@@ -224,9 +224,12 @@ struct TpSrc {
 // ST / W: compile-time stage / width (0 = take the runtime argument); the
 // chains the compressor runs are instantiated with both fixed, so each kernel
 // holds only its own width's load/store code.
+// done != null: each completed tile (all its stores fenced) bumps *done, and
+// the CTA holding the last tile also publishes the level's sizes (k_reduce_tail).
 template <class Src, typename WT, int ST = 0, int W = 0>
 __device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage_rt, int width_rt, uint8_t* bitmap,
-                             uint8_t* payload, unsigned long long* lb, BmLevel* lv, uint8_t* stg) {
+                             uint8_t* payload, unsigned long long* lb, BmLevel* lv, uint8_t* stg,
+                             unsigned long long* done = nullptr) {
   const int stage = ST ? ST : stage_rt;
   const int width = W ? W : width_rt;
   __shared__ unsigned long long sh[33];
@@ -316,8 +319,18 @@ __device__ void reduce_tiles(const Src& src, unsigned long long nw, int stage_rt
         }
       }
     }
-    if (tile == ntiles - 1 && threadIdx.x == 0) lv->kept = base_sh + total;
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+      lv->kept = base_sh + total;
+      if (done) {
+        lv->orig = nw;
+        lv->nwords = nw;
+        lv->bm_len = cdiv(nw, 8);
+        lv->active = 1;
+      }
+    }
+    if (done) __threadfence();
     __syncthreads();
+    if (done && threadIdx.x == 0) atomicAdd(done, 1ull);
   }
 }
 
@@ -462,6 +475,74 @@ __global__ void k_chain_assemble(int stage, int width0, BmState* bm, uint8_t* co
   for (unsigned long long i = end + tid; i < ((end + 7) & ~7ull) + 8; i += nth) dst[i] = 0;
 }
 
+// Levels 1..3 of a chain and the record assembly in ONE launch (they were
+// four: ~7 us of fixed latency each on small records).  Tiles are handed out
+// per level by that level's ticket; a CTA that finds its level's tickets
+// exhausted waits until every tile of the level has completed before reading
+// the level's sizes.  Tiles are only ever held by running CTAs, so the wait
+// cannot deadlock whatever the residency.  Then every CTA lays out the record
+// and copies its share (k_chain_assemble's body).
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(RD_THREADS, 4)
+    k_reduce_tail(int stage, int width0, BmState* bm, uint8_t* const* bitmaps, uint8_t* const* payloads,
+                  unsigned long long* lb_ws, unsigned long long lb_stride, uint8_t* out,
+                  const unsigned long long* dst_off_dev, unsigned long long* rec_len_out) {
+  __shared__ __align__(16) uint8_t stg[RD_TILE];
+  __shared__ ChainLayout L;
+  __shared__ BmState sbm;
+  for (int level = 1; level <= 3; level++) {
+    BmLevel* p = &bm->lv[level - 1];
+    // written by k_reduce0 (level 1) or by this kernel before the wait below
+    const int active = __ldcg(&p->active);
+    const unsigned long long nw = __ldcg(&p->bm_len);
+    if (!active || nw <= 19) break;
+    BmLevel* lv = &bm->lv[level];
+    MemSrc src{bitmaps[level - 1], nw, 1};
+    reduce_tiles<MemSrc, uint32_t, 2, 1>(src, nw, 2, 1, bitmaps[level], payloads[level], lb_ws + level * lb_stride, lv,
+                                         stg, &lv->tiles_done);
+    if (threadIdx.x == 0) {
+      const unsigned long long nt = cdiv(nw, RD_TILE);
+      while (ld_acquire_u64(&lv->tiles_done) < nt) __nanosleep(64);
+    }
+    __syncthreads();
+  }
+  // record layout from an L2-fresh copy of the level table
+  if (threadIdx.x < (int)(sizeof(BmState) / 8))
+    reinterpret_cast<unsigned long long*>(&sbm)[threadIdx.x] =
+        __ldcg(reinterpret_cast<const unsigned long long*>(bm) + threadIdx.x);
+  __syncthreads();
+  if (threadIdx.x == 0) chain_layout(&sbm, width0, &L);
+  __syncthreads();
+  uint8_t* dst = out + (dst_off_dev ? *dst_off_dev : 0ull);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int k = 0; k <= L.last; k++) {
+      uint8_t* h = dst + L.off[k];
+      h[0] = (uint8_t)(k == 0 ? stage : 2);
+      h[1] = (uint8_t)(k == 0 ? width0 : 1);
+      st_bytes(h + 2, sbm.lv[k].orig, 8);
+      h[10] = (uint8_t)L.flag[k];
+      st_bytes(h + 11, L.sec_len[k], 8);
+      bm->lv[k].flag = L.flag[k];
+      bm->lv[k].rec_len = L.rec_len[k];
+    }
+    *rec_len_out = L.rec_len[0];
+  }
+  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long nth = (unsigned long long)gridDim.x * blockDim.x;
+  copy_to_unaligned(dst + L.off[L.last] + 19, bitmaps[L.last], sbm.lv[L.last].bm_len, tid, nth);
+  for (int k = 0; k <= L.last; k++) {
+    const int w = k == 0 ? width0 : 1;
+    copy_to_unaligned(dst + L.pay_off[k], payloads[k], sbm.lv[k].kept * w, tid, nth);
+  }
+  const unsigned long long end = L.rec_len[0];
+  for (unsigned long long i = end + tid; i < ((end + 7) & ~7ull) + 8; i += nth) dst[i] = 0;
+}
+
 struct ChainPtrs {
   uint8_t* bitmap[4];
   uint8_t* payload[4];
@@ -523,6 +604,13 @@ void launch_reduce_chain_impl(int stage, int width, int src_kind, const uint8_t*
       break;
   }
   (*launches)++;
+  static const bool split_tail = getenv("HB_SPLIT_TAIL") != nullptr;  // the four-launch form (variant tests)
+  if (!split_tail) {
+    k_reduce_tail<<<PERSIST_CTAS, RD_THREADS, 0, s>>>(stage, width, bm, dev_ptr_tables, dev_ptr_tables + 4, lb_ws,
+                                                      lb_stride, rec_out, dst_off_dev, rec_len_dev);
+    (*launches)++;
+    return;
+  }
   unsigned long long words = cdiv(max_words, 8);
   for (int k = 1; k <= 3; k++) {
     const unsigned g = persist_grid(cdiv(words, RD_TILE));

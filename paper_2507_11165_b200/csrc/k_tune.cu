@@ -100,14 +100,15 @@ __device__ double pw_leaf(const double* a, int n) {
 }
 
 // enumerate leaves of the pairwise recursion in order (explicit stack)
-__device__ int pw_leaves(int n, int* ls, int* ln) {
+template <typename I>
+__device__ int pw_leaves(int n, I* ls, I* ln) {
   int stk_s[32], stk_n[32], sp = 0, nl = 0;
   stk_s[sp] = 0, stk_n[sp] = n, sp++;
   while (sp) {
     sp--;
     const int s0 = stk_s[sp], n0 = stk_n[sp];
     if (n0 <= 128) {
-      ls[nl] = s0, ln[nl] = n0, nl++;
+      ls[nl] = (I)s0, ln[nl] = (I)n0, nl++;
     } else {
       int n2 = n0 / 2;
       n2 -= n2 % 8;
@@ -141,15 +142,17 @@ __device__ __forceinline__ int qdiv(int a, int b, float rb) {
 // tuning.py:135-140 for one level, run by the first warp of the CTA that
 // finishes the level last (k_tune_level): Neumaier sum of the block errors per
 // config, (err, index) argmin, winner handed to the next level.
-__device__ void tune_select(int nb, int level, const double* berr, DevState* st, uint8_t* host_cfg,
+// `x` holds the 4 x nb block errors (staged in shared memory by the caller:
+// a serial loop of dependent L2 loads cost ~20 us per level).
+__device__ void tune_select(int nb, int level, const double* berr, bool staged, DevState* st, uint8_t* host_cfg,
                             cudaGraphConditionalHandle cond) {
   __shared__ double e[4];
   const int ci = threadIdx.x;
   if (ci < 4) {
     const double* x = berr + ci * nb;
-    double f = __dadd_rn(0.0, __ldcg(&x[0])), c = 0.0;  // sum() starts from int 0
+    double f = __dadd_rn(0.0, staged ? x[0] : __ldcg(&x[0])), c = 0.0;  // sum() starts from int 0
     for (int i = 1; i < nb; i++) {
-      const double xi = __ldcg(&x[i]);
+      const double xi = staged ? x[i] : __ldcg(&x[i]);
       const double t = __dadd_rn(f, xi);
       if (fabs(f) >= fabs(xi))
         c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), xi));
@@ -187,37 +190,63 @@ __global__ void __launch_bounds__(TUNE_THREADS)
   extern __shared__ double tsm[];
   const int bn = b0 * b1 * b2;
   double* g = tsm;
-  double* diff = tsm + bn;
+  double* diff = tsm + bn;  // two halves: sub-steps alternate (a sub-step has <= bn/2 targets)
   T* orig = reinterpret_cast<T*>(diff + bn);
-  __shared__ double leaf[160];
-  __shared__ int lstart[160], llen[160];
-  __shared__ int nleaf;
+  // pairwise-sum leaves of every sub-step (a sub-step has <= bn/2 <= 5120
+  // targets and leaves of >= 57, so <= 90 leaves)
+  constexpr int TL = 96;
+  __shared__ uint16_t lstart[7][TL], llen[7][TL];
+  __shared__ double leafv[7][TL];
+  __shared__ int nleaf[7];
   const int ci = blockIdx.x / nb, b = blockIdx.x % nb;
   // original block values (tuning.py:111-112): gathered from the field at the
-  // top level (and kept compact in borig), read back contiguously below it
+  // top level (and kept compact in borig), read back contiguously below it.
+  // Loads are issued in batches of GB per thread (one memory latency per batch).
+  constexpr int GB = 8;
+  const size_t set_stride = (size_t)4 * nb * bn;
   if (level == top) {
     const unsigned long long ox = origins[3 * b], oy = origins[3 * b + 1], oz = origins[3 * b + 2];
     const float r2 = 1.0f / (float)b2, r12 = 1.0f / (float)(b1 * b2);
-    for (int i = threadIdx.x; i < bn; i += blockDim.x) {
-      const int x = qdiv(i, b1 * b2, r12), yz = i - x * b1 * b2, y = qdiv(yz, b2, r2), z = yz - y * b2;
-      const T v = field[((ox + x) * fd1 + oy + y) * fd2 + oz + z];
-      orig[i] = v;
-      if (ci == 0) borig[(size_t)b * bn + i] = v;
+    for (int i0 = threadIdx.x; i0 < bn; i0 += GB * blockDim.x) {
+      T v[GB];
+#pragma unroll
+      for (int k = 0; k < GB; k++) {
+        const int i = i0 + k * blockDim.x;
+        if (i < bn) {
+          const int x = qdiv(i, b1 * b2, r12), yz = i - x * b1 * b2, y = qdiv(yz, b2, r2), z = yz - y * b2;
+          v[k] = field[((ox + x) * fd1 + oy + y) * fd2 + oz + z];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < GB; k++) {
+        const int i = i0 + k * blockDim.x;
+        if (i < bn) {
+          orig[i] = v[k];
+          g[i] = (double)v[k];
+          if (ci == 0) borig[(size_t)b * bn + i] = v[k];
+        }
+      }
     }
   } else {
-    for (int i = threadIdx.x; i < bn; i += blockDim.x) orig[i] = borig[(size_t)b * bn + i];
-  }
-  // state carried from the previous level's winner (tuning.py:140)
-  const size_t set_stride = (size_t)4 * nb * bn;
-  if (level == top) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < bn; i += blockDim.x) g[i] = (double)orig[i];
-  } else {
+    // state carried from the previous level's winner (tuning.py:140)
     const int w = st->tune_winner[level];  // winner of level+1
     const double* src = trials + (size_t)((level + 1) & 1) * set_stride + ((size_t)w * nb + b) * bn;
-    for (int i = threadIdx.x; i < bn; i += blockDim.x) g[i] = src[i];
+    const T* bo = borig + (size_t)b * bn;
+    for (int i0 = threadIdx.x; i0 < bn; i0 += GB * blockDim.x) {
+      T v[GB];
+      double u[GB];
+#pragma unroll
+      for (int k = 0; k < GB; k++) {
+        const int i = i0 + k * blockDim.x;
+        if (i < bn) v[k] = bo[i], u[k] = src[i];
+      }
+#pragma unroll
+      for (int k = 0; k < GB; k++) {
+        const int i = i0 + k * blockDim.x;
+        if (i < bn) orig[i] = v[k], g[i] = u[k];
+      }
+    }
   }
-  __syncthreads();
   const uint8_t cb = c_choice[ci];
   const bool linear = cb & 1, seq1d = (cb >> 1) & 1;
   const double eb = st->eb, two_eb = st->two_eb, inv_two_eb = __ddiv_rn(1.0, two_eb);
@@ -230,13 +259,22 @@ __global__ void __launch_bounds__(TUNE_THREADS)
   if (threadIdx.x == 0) s_nss = block_steps(dims, level, seq1d, s_ss);
   __syncthreads();
   const int nss = s_nss;
+  // leaf tables, one thread per sub-step (read after the first sub-step's barrier)
+  if (threadIdx.x < nss) {
+    const SubStep& S = s_ss[threadIdx.x];
+    nleaf[threadIdx.x] = pw_leaves(S.count[0] * S.count[1] * S.count[2], lstart[threadIdx.x], llen[threadIdx.x]);
+  }
   const int s = 1 << (level - 1);
-  double total = 0.0;
+  // One barrier per sub-step: it publishes the sub-step's reconstructions
+  // (the next sub-step's stencil taps) and its |orig - pred| half.  The leaf
+  // sums of sub-step t run before the barrier of t+1, which precedes the next
+  // write of that half (sub-step t+2); the pairwise combines run at the end.
   for (int t = 0; t < nss; t++) {
     const SubStep S = s_ss[t];
     const int n = S.count[0] * S.count[1] * S.count[2];
     const int c12 = S.count[1] * S.count[2];
     const float r2 = 1.0f / (float)S.count[2], r12 = 1.0f / (float)c12;
+    double* dd = diff + (t & 1) * (bn / 2);
     for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
       int c[3];
       const int q0 = qdiv(idx, c12, r12), rem = idx - q0 * c12, q1 = qdiv(rem, S.count[2], r2);
@@ -263,34 +301,31 @@ __global__ void __launch_bounds__(TUNE_THREADS)
       }
       const double pred = S.k == 1 ? pv[0] : combine_axes(S.k, pv, ov);
       const double o = (double)orig[lin];
-      diff[idx] = fabs(__dsub_rn(o, pred));
+      dd[idx] = fabs(__dsub_rn(o, pred));
       double r;
       quantize_fast<sizeof(T) == 4>(o, pred, eb, two_eb, inv_two_eb, &r);
       g[lin] = r;
     }
     __syncthreads();
-    if (threadIdx.x == 0) nleaf = pw_leaves(n, lstart, llen);
-    __syncthreads();
     // each leaf on 8 lanes: lane j owns numpy's accumulator r[j] (column j)
-    for (int base = 0; base < nleaf; base += TUNE_THREADS / 8) {
+    const int nl = nleaf[t];
+    for (int base = 0; base < nl; base += TUNE_THREADS / 8) {
       const int li = base + (int)(threadIdx.x >> 3), j = threadIdx.x & 7;
       double r = 0.0;
       int ln = 0;
-      const double* a = diff;
-      if (li < nleaf) {
-        ln = llen[li];
-        a = diff + lstart[li];
+      const double* a = dd;
+      if (li < nl) {
+        ln = llen[t][li];
+        a = dd + lstart[t][li];
         if (ln >= 8) {
           r = a[j];
           for (int i = 8; i < ln - (ln % 8); i += 8) r = __dadd_rn(r, a[i + j]);
         }
       }
-      const unsigned gmask = 0xFFu << (threadIdx.x & 24);
       double rr[8];
 #pragma unroll
       for (int q = 0; q < 8; q++) rr[q] = __shfl_sync(0xffffffffu, r, (threadIdx.x & 24) + q);
-      (void)gmask;
-      if (li < nleaf && j == 0) {
+      if (li < nl && j == 0) {
         double res;
         if (ln < 8) {
           res = 0.0;
@@ -300,15 +335,9 @@ __global__ void __launch_bounds__(TUNE_THREADS)
                           __dadd_rn(__dadd_rn(rr[4], rr[5]), __dadd_rn(rr[6], rr[7])));
           for (int i = ln - (ln % 8); i < ln; i++) res = __dadd_rn(res, a[i]);
         }
-        leaf[li] = res;
+        leafv[t][li] = res;
       }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int cur = 0;
-      total = __dadd_rn(total, pw_combine(n, leaf, &cur));
-    }
-    __syncthreads();
   }
   double* dst = trials + (size_t)(level & 1) * set_stride + ((size_t)ci * nb + b) * bn;
   for (int i = threadIdx.x; i < bn; i += blockDim.x) dst[i] = g[i];
@@ -316,6 +345,12 @@ __global__ void __launch_bounds__(TUNE_THREADS)
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
+    // the block's error: sum over sub-steps (in order) of numpy's pairwise sum
+    double total = 0.0;
+    for (int t = 0; t < nss; t++) {
+      int cur = 0;
+      total = __dadd_rn(total, pw_combine(s_ss[t].count[0] * s_ss[t].count[1] * s_ss[t].count[2], leafv[t], &cur));
+    }
     berr[ci * nb + b] = total;
     __threadfence();
     last = atomicAdd(done, 1u) == gridDim.x - 1;
@@ -323,7 +358,14 @@ __global__ void __launch_bounds__(TUNE_THREADS)
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x < 32) tune_select(nb, level, berr, st, host_cfg, cond);
+  // every CTA's block errors into shared memory with parallel loads (the
+  // trial grid is no longer needed), then one warp runs the ordered sums
+  const bool staged = (size_t)4 * nb * 8 <= (size_t)bn * (16 + sizeof(T));
+  if (staged) {
+    for (int i = threadIdx.x; i < 4 * nb; i += blockDim.x) tsm[i] = __ldcg(&berr[i]);
+    __syncthreads();
+  }
+  if (threadIdx.x < 32) tune_select(nb, level, staged ? tsm : berr, staged, st, host_cfg, cond);
   if (threadIdx.x == 0) *done = 0;  // ready for the next level / call
 }
 

@@ -12,6 +12,8 @@ others so none of them ships untested:
   HB_MARCH=1         axis-0 marching level kernel (k_march.cu) for multidim 3D levels
   HB_SWEEP=2 / 1     level 1 as one slab-ordered sweep (persistent / one item per CTA)
                      instead of the seven per-class TMA passes
+  HB_SPLIT_TAIL      reducer chain levels 1..3 and the record assembly as four
+                     launches instead of the fused k_reduce_tail
 """
 import os
 import subprocess
@@ -35,6 +37,7 @@ VARIANTS = {
     "march": {"HB_MARCH": "1"},
     "sweep": {"HB_SWEEP": "2"},
     "sweep-one": {"HB_SWEEP": "1"},
+    "split-tail": {"HB_SPLIT_TAIL": "1"},
 }
 
 
