@@ -912,7 +912,7 @@ static int compress_impl(hb_ctx* ctx, const void* field, int prec, const uint64_
   const size_t o_rre4 = L.take(rre4_max + 64);
   // look-back workspaces
   const unsigned long long lb_oc = lb_entries(cdiv(N, 32), 8192);
-  const unsigned long long lb_he = lb_entries(N, 8192);
+  const unsigned long long lb_he = lb_entries(N, HE_TILE_SYMS);
   const unsigned long long lb_c1 = lb_entries(w1, 8192), lb_c2 = lb_entries(w2 ? w2 : 1, 8192);
   const size_t o_lb = L.take((lb_oc + lb_he + 4 * lb_c1 + 4 * lb_c2) * 8);
   const size_t lb_bytes = (lb_oc + lb_he + 4 * lb_c1 + 4 * lb_c2) * 8;

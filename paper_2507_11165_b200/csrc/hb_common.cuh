@@ -189,6 +189,37 @@ __device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* 
   return excl;
 }
 
+// The wait half of lookback_warp for a tile that already published its
+// aggregate (t > 0): whole warp, returns the exclusive prefix and publishes
+// the inclusive one.
+__device__ __forceinline__ unsigned long long lookback_wait(unsigned long long* status, unsigned long long t,
+                                                            unsigned long long agg) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long excl = 0;
+  long long base = (long long)t - 1;
+  while (true) {
+    const long long j = base - lane;
+    unsigned long long s = j >= 0 ? ld_volatile(&status[j]) : LB_INC;
+    while (__any_sync(0xffffffffu, (s >> 62) == 0)) {
+      __nanosleep(32);  // back off: spinning warps steal issue slots from the producers
+      if ((s >> 62) == 0) s = ld_volatile(&status[j]);
+    }
+    const unsigned inc = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+    if (inc) {
+      const int first = __ffs(inc) - 1;
+      excl += warp_sum<unsigned long long>(lane <= first ? (s & LB_MASK) : 0ull);
+      break;
+    }
+    excl += warp_sum<unsigned long long>(s & LB_MASK);
+    base -= 32;
+  }
+  if (lane == 0) {
+    __threadfence();
+    atomicExch(&status[t], LB_INC | (excl + agg));
+  }
+  return excl;
+}
+
 // ordered encodings for float min/max atomics
 __device__ __forceinline__ unsigned long long ord_bits(double v) {
   unsigned long long b = (unsigned long long)__double_as_longlong(v);

@@ -130,6 +130,8 @@ void launch_reduce_chain_impl(int stage, int width, int src_kind, const uint8_t*
                               cudaStream_t s, int* launches);
 void launch_hist(const uint8_t* in, unsigned long long n, DevState* st, cudaStream_t s, int* launches);
 void launch_huffman_build(DevState* st, unsigned long long n, uint8_t* hf_rec, cudaStream_t s, int* launches);
+// symbols per Huffman-encode tile (one look-back entry each)
+constexpr unsigned long long HE_TILE_SYMS = 4096;
 void launch_huffman_encode(const uint8_t* seq, unsigned long long n, uint8_t* hf_rec, unsigned long long* lb_ws,
                            DevState* st, cudaStream_t s, int* launches);
 void launch_stream_offset(unsigned long long base, int prec, DevState* st, cudaStream_t s, int* launches);

@@ -791,149 +791,230 @@ __global__ void k_huff_zero(uint32_t* rec_words, DevState* st) {
     rec_words[i] = 0;
 }
 
-constexpr int HE_SYMS = 32;  // symbols per thread
-constexpr int HE_TILE = 256 * HE_SYMS;
-constexpr int HE_SMEM_WORDS = HE_TILE / 4 + 64;  // 8 bits/symbol; larger tiles take the global path
+constexpr int HE_SYMS = 32;                    // symbols per lane per round
+constexpr int HE_ROUNDS = 4;                   // rounds of 32 x 32 symbols per warp tile
+constexpr int HE_WTILE = 32 * HE_SYMS * HE_ROUNDS;  // symbols per warp tile (== HE_TILE_SYMS, hb_kernels.h)
+constexpr int HE_WARPS = 8;                    // warps per CTA
+constexpr int HE_BUF = HE_WTILE / 4 + 2;       // words per warp buffer: <= 8 bits/symbol (+ spill word)
+static_assert(HE_WTILE == HE_TILE_SYMS, "look-back workspace sizing");
 
-// Each tile (8192 symbols) packs its codes MSB-first into a shared-memory bit
-// buffer (smem atomics only where two threads share a word), then streams the
-// whole-word range out with coalesced stores; only the first and last word of
-// a tile can be shared with a neighbouring tile and use a global atomicOr
-// (payload zeroed beforehand).
-__global__ void __launch_bounds__(256) k_huff_encode(const uint8_t* __restrict__ in, unsigned long long n,
-                                                     uint32_t* rec_words, unsigned long long* lb, DevState* st) {
-  extern __shared__ uint32_t hbuf[];
-  __shared__ unsigned long long stab[256];  // code | len << 56
-  __shared__ unsigned long long sh[33];
-  __shared__ unsigned long long tile_sh, base_sh;
-  {
-    const unsigned long long L = st->hf_len[threadIdx.x];
-    stab[threadIdx.x] = st->hf_code[threadIdx.x] | (L << 56);
+// MSB-first OR of one code into a big-endian-bit word array (bits [pos, pos+L))
+template <bool GLOBAL>
+__device__ __forceinline__ void he_put(uint32_t* words, unsigned long long pos, int L, unsigned long long c) {
+  const unsigned long long end = pos + L;
+  unsigned long long wi = (end - 1) >> 5;
+  const int r = (int)(end & 31);
+  int left = L, first = r ? r : 32;
+  while (left > 0) {
+    const int take = left < first ? left : first;
+    const uint32_t be = (uint32_t)(c & ((1ull << take) - 1)) << (32 - first);
+    if (GLOBAL)
+      atomicOr(&words[wi], __byte_perm(be, 0, 0x0123));
+    else
+      atomicOr(&words[wi], be);
+    c >>= take;
+    left -= take;
+    wi--;
+    first = 32;
   }
-  __syncthreads();
-  const unsigned long long ntiles = cdiv(n, HE_TILE);
-  for (;;) {
-    if (threadIdx.x == 0) tile_sh = atomicAdd(lb, 1ull);
-    __syncthreads();
-    const unsigned long long tile = tile_sh;
-    if (tile >= ntiles) break;
-    const unsigned long long s0 = tile * HE_TILE + (unsigned long long)threadIdx.x * HE_SYMS;
-    const int cnt = s0 >= n ? 0 : (s0 + HE_SYMS <= n ? HE_SYMS : (int)(n - s0));
-    uint32_t w[8];
-    if (cnt == HE_SYMS) {
-      const uint4* p = reinterpret_cast<const uint4*>(in + s0);
-      const uint4 a = p[0], b = p[1];
-      w[0] = a.x, w[1] = a.y, w[2] = a.z, w[3] = a.w, w[4] = b.x, w[5] = b.y, w[6] = b.z, w[7] = b.w;
-    } else {
+}
+
+// the 32 symbols of one lane in one round, zero past the end
+__device__ __forceinline__ int he_load(const uint8_t* __restrict__ in, unsigned long long n, unsigned long long s0,
+                                       uint32_t (&w)[8]) {
+  const int cnt = s0 >= n ? 0 : (s0 + HE_SYMS <= n ? HE_SYMS : (int)(n - s0));
+  if (cnt == HE_SYMS) {
+    const uint4* p = reinterpret_cast<const uint4*>(in + s0);
+    const uint4 a = p[0], b = p[1];
+    w[0] = a.x, w[1] = a.y, w[2] = a.z, w[3] = a.w, w[4] = b.x, w[5] = b.y, w[6] = b.z, w[7] = b.w;
+  } else {
 #pragma unroll
-      for (int q = 0; q < 8; q++) {
-        w[q] = 0;
-        for (int k = 0; k < 4; k++)
-          if (q * 4 + k < cnt) w[q] |= (uint32_t)in[s0 + q * 4 + k] << (8 * k);
+    for (int q = 0; q < 8; q++) {
+      w[q] = 0;
+      for (int k = 0; k < 4; k++)
+        if (q * 4 + k < cnt) w[q] |= (uint32_t)in[s0 + q * 4 + k] << (8 * k);
+    }
+  }
+  return cnt;
+}
+
+constexpr int HE_PRIV = 8;  // words of a lane's round kept in shared memory (denser lanes re-walk)
+
+// One lane's round: its 32 codes through a 64-bit bit writer into the lane's
+// private words (left-aligned, MSB-first), returns the round's bit count and
+// whether they all fit the private words.  Codes <= 32 bits.
+template <bool FULL>
+__device__ __forceinline__ unsigned he_pack_lane(const uint32_t (&w)[8], int cnt, const unsigned long long* stab,
+                                                 uint32_t* priv, bool& fits) {
+  uint64_t acc = 0;
+  unsigned ab = 0, nw = 0;
+  auto put32 = [&](uint32_t c, unsigned L) {  // L <= 32, ab < 32 on entry
+    acc |= (uint64_t)c << (64 - ab - L);
+    ab += L;
+    if (ab >= 32) {
+      if (nw < HE_PRIV) priv[nw * 32] = (uint32_t)(acc >> 32);
+      nw++;
+      acc <<= 32;
+      ab -= 32;
+    }
+  };
+#pragma unroll
+  for (int k = 0; k < HE_SYMS; k++) {
+    if (FULL || k < cnt) {
+      const unsigned long long e = stab[(w[k >> 2] >> (8 * (k & 3))) & 0xFF];
+      const unsigned L = (unsigned)(e >> 56);
+      put32((uint32_t)e, L);
+    }
+  }
+  const unsigned nb = nw * 32 + ab;
+  if (ab) {
+    if (nw < HE_PRIV) priv[nw * 32] = (uint32_t)(acc >> 32);
+    nw++;
+  }
+  fits = nw <= HE_PRIV;
+  return nb;
+}
+
+// Warp-granular tiles: each warp takes a 4096-symbol tile by ticket (four
+// rounds of 32 lanes x 32 symbols).  Per round every lane runs its codes
+// through a register bit writer into private shared-memory words, a warp
+// scan places the lanes, and each lane ORs its words into the warp's tile
+// buffer at the tile-relative bit offset (no CTA barrier anywhere).  Then the
+// tile publishes its bit count and resolves its global bit offset by
+// decoupled look-back (hb_common.cuh), and streams the buffer out shifted by
+// that offset (funnel shift per word, coalesced stores, the buffer re-zeroed
+// on the way).  Only the first and last word of a tile can share bits with a
+// neighbouring tile (global atomicOr into the pre-zeroed payload).  Rounds
+// past the buffer's capacity (> 8 bits/symbol) OR straight into global
+// memory after the look-back.
+// long_codes: some code exceeds 32 bits -- every lane takes the per-code path
+__device__ __forceinline__ void he_tiles(const uint8_t* __restrict__ in, unsigned long long n, uint32_t* rec_words,
+                                         unsigned long long* lb, const unsigned long long* stab,
+                                         const uint8_t* slen, uint32_t* buf, uint32_t* priv, unsigned* sx,
+                                         bool long_codes) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long* status = lb + 1;
+  const unsigned long long ntiles = cdiv(n, HE_WTILE);
+  for (;;) {
+    unsigned long long tile = 0;
+    if (lane == 0) tile = atomicAdd(lb, 1ull);
+    tile = __shfl_sync(0xffffffffu, tile, 0);
+    if (tile >= ntiles) break;
+    const unsigned long long t0 = tile * HE_WTILE + (unsigned long long)lane * HE_SYMS;
+    // pass 1: code lengths only -> per-round lane offsets, tile total; the
+    // aggregate is published before any packing so successors' look-backs
+    // rarely wait
+    unsigned total = 0, buf_bits = 0;
+    int rd = HE_ROUNDS;  // first round that goes straight to global memory
+#pragma unroll 1
+    for (int r = 0; r < HE_ROUNDS; r++) {
+      uint32_t w[8];
+      const int cnt = he_load(in, n, t0 + r * 32 * HE_SYMS, w);
+      unsigned nb = 0;
+      if (cnt == HE_SYMS) {
+#pragma unroll
+        for (int k = 0; k < HE_SYMS; k++) nb += slen[(w[k >> 2] >> (8 * (k & 3))) & 0xFF];
+      } else {
+        for (int k = 0; k < cnt; k++) nb += slen[(w[k >> 2] >> (8 * (k & 3))) & 0xFF];
+      }
+      const unsigned inc = warp_incl_scan<unsigned>(nb);
+      sx[r * 32 + lane] = total + inc - nb;  // the lane's first bit of round r
+      total += __shfl_sync(0xffffffffu, inc, 31);
+      if (rd == HE_ROUNDS && total > (unsigned)(HE_BUF - 2) * 32) rd = r;  // warp-uniform
+      if (r < rd) buf_bits = total;
+    }
+    if (lane == 0) {
+      if (tile == 0) {
+        __threadfence();
+        atomicExch(&status[0], LB_INC | total);
+      } else {
+        atomicExch(&status[tile], LB_AGG | total);
       }
     }
-    unsigned nb = 0;
-#pragma unroll
-    for (int k = 0; k < HE_SYMS; k++)
-      if (k < cnt) nb += (unsigned)(stab[(w[k >> 2] >> (8 * (k & 3))) & 0xFF] >> 56);
-    unsigned long long total;
-    const unsigned long long excl = block_excl_scan<unsigned long long>(nb, sh, &total);
-    if (threadIdx.x < 32) {
-      const unsigned long long ex_ = lookback_warp(lb + 1, tile, total);
-      if (threadIdx.x == 0) base_sh = ex_;
+    // pass 2: pack the rounds that fit the tile buffer
+#pragma unroll 1
+    for (int r = 0; r < rd; r++) {
+      uint32_t w[8];
+      const int cnt = he_load(in, n, t0 + r * 32 * HE_SYMS, w);
+      bool fits;
+      const unsigned e0 = sx[r * 32 + lane];
+      unsigned nb = 0;
+      if (long_codes)
+        fits = false;
+      else if (cnt == HE_SYMS)
+        nb = he_pack_lane<true>(w, cnt, stab, priv + lane, fits);
+      else
+        nb = he_pack_lane<false>(w, cnt, stab, priv + lane, fits);
+      if (fits) {
+        const unsigned b = e0 & 31, wb = e0 >> 5, nwl = (nb + 31) >> 5;
+        for (unsigned i = 0; i < nwl; i++) {
+          const uint32_t v = priv[lane + 32 * i];
+          if (v) {
+            atomicOr(&buf[wb + i], v >> b);
+            if (b && (v << (32 - b))) atomicOr(&buf[wb + i + 1], v << (32 - b));
+          }
+        }
+      } else {  // a dense lane: re-walk its codes
+        unsigned long long pos = e0;
+        for (int k = 0; k < HE_SYMS; k++) {
+          const unsigned long long e = k < cnt ? stab[(w[k >> 2] >> (8 * (k & 3))) & 0xFF] : 0ull;
+          const int L = (int)(e >> 56);
+          const unsigned long long c = e & ((1ull << 56) - 1);
+          if (c) he_put<false>(buf, pos, L, c);
+          pos += L;
+        }
+      }
+      __syncwarp();  // private words reused by the next round
     }
-    __syncthreads();
-    const unsigned long long tstart = 274ull * 8 + base_sh;  // tile's first bit in the record
-    const int shift0 = (int)(tstart & 31);
+    const unsigned long long base = tile == 0 ? 0ull : lookback_wait(status, tile, total);
+    const unsigned long long tstart = 274ull * 8 + base;  // the tile's first bit in the record
+    const int s = (int)(tstart & 31);
     const unsigned long long w0 = tstart >> 5;
-    const unsigned long long nwords = (shift0 + total + 31) >> 5;
-    const bool in_smem = nwords <= HE_SMEM_WORDS;
-    if (in_smem)
-      for (unsigned i = threadIdx.x; i < nwords; i += blockDim.x) hbuf[i] = 0;
-    __syncthreads();
-    // OR only the non-zero bits: the all-zero canonical code (the most
-    // frequent symbol) just advances the bit position
-    unsigned long long pos = in_smem ? shift0 + excl : tstart + excl;
-    if (in_smem && nb <= 128) {
-      // common case: the thread's whole bit string fits 128 bits -- build it
-      // in registers (branch-free shifts) and OR it in as <= 5 aligned words
-      uint64_t ah = 0, al = 0;
-#pragma unroll
+    const unsigned nout = buf_bits ? (s + buf_bits + 31) >> 5 : 0;
+    for (unsigned j = lane; j < nout; j += 32) {
+      const uint32_t v = s ? ((j ? buf[j - 1] << (32 - s) : 0u) | (buf[j] >> s)) : buf[j];
+      const uint32_t le = __byte_perm(v, 0, 0x0123);
+      if (j == 0 || j == nout - 1) {
+        if (v) atomicOr(&rec_words[w0 + j], le);
+      } else {
+        rec_words[w0 + j] = le;
+      }
+    }
+    __syncwarp();
+    for (unsigned j = lane; j < nout; j += 32) buf[j] = 0;  // clean for the next tile
+    __syncwarp();
+#pragma unroll 1
+    for (int r = rd; r < HE_ROUNDS; r++) {
+      uint32_t w[8];
+      const int cnt = he_load(in, n, t0 + r * 32 * HE_SYMS, w);
+      unsigned long long pos = tstart + sx[r * 32 + lane];
       for (int k = 0; k < HE_SYMS; k++) {
         const unsigned long long e = k < cnt ? stab[(w[k >> 2] >> (8 * (k & 3))) & 0xFF] : 0ull;
         const int L = (int)(e >> 56);
-        const uint64_t c = e & ((1ull << 56) - 1);
-        if (L) {
-          ah = (ah << L) | (al >> (64 - L));
-          al = (al << L) | c;
-        }
-      }
-      if (nb) {
-        // left-align to 128 bits, then shift right by the in-word bit offset
-        const int sh = 128 - (int)nb;
-        uint64_t H, Lo;
-        if (sh >= 64) {
-          H = al << (sh - 64);
-          Lo = 0;
-        } else if (sh > 0) {
-          H = (ah << sh) | (al >> (64 - sh));
-          Lo = al << sh;
-        } else {
-          H = ah;
-          Lo = al;
-        }
-        const int b = (int)(pos & 31);
-        const uint64_t T0 = H >> b, T1 = b ? (H << (64 - b)) | (Lo >> b) : Lo, T2 = b ? Lo << (64 - b) : 0ull;
-        const uint32_t wd[5] = {(uint32_t)(T0 >> 32), (uint32_t)T0, (uint32_t)(T1 >> 32), (uint32_t)T1,
-                                (uint32_t)(T2 >> 32)};
-        const unsigned long long wi0 = pos >> 5;
-        const int nwd = (b + (int)nb + 31) >> 5;
-#pragma unroll
-        for (int q = 0; q < 5; q++)
-          if (q < nwd && wd[q]) atomicOr(&hbuf[wi0 + q], wd[q]);
-      }
-    } else
-#pragma unroll
-    for (int k = 0; k < HE_SYMS; k++) {
-      const unsigned long long e = k < cnt ? stab[(w[k >> 2] >> (8 * (k & 3))) & 0xFF] : 0ull;
-      const int L = (int)(e >> 56);
-      const unsigned long long c = e & ((1ull << 56) - 1);
-      if (c) {
-        // bits of c end at pos + L; split over at most 3 words
-        const unsigned long long end = pos + L;
-        unsigned long long wi = (end - 1) >> 5;
-        const int r = (int)(end & 31);  // bits of the last word used
-        unsigned long long v = c;
-        int left = L;
-        int first = r ? r : 32;
-        while (left > 0) {
-          const int take = left < first ? left : first;
-          const uint32_t chunk = (uint32_t)(v & ((1ull << take) - 1));
-          const uint32_t be = chunk << (32 - first);  // place within the word (MSB-first)
-          if (in_smem)
-            atomicOr(&hbuf[wi], be);
-          else
-            atomicOr(&rec_words[wi], __byte_perm(be, 0, 0x0123));
-          v >>= take;
-          left -= take;
-          wi--;
-          first = 32;
-        }
-      }
-      pos += L;
-    }
-    __syncthreads();
-    if (in_smem) {
-      for (unsigned i = threadIdx.x; i < nwords; i += blockDim.x) {
-        const uint32_t le = __byte_perm(hbuf[i], 0, 0x0123);
-        if (i == 0 || i == nwords - 1)
-          atomicOr(&rec_words[w0 + i], le);
-        else
-          rec_words[w0 + i] = le;
+        const unsigned long long c = e & ((1ull << 56) - 1);
+        if (c) he_put<true>(rec_words, pos, L, c);
+        pos += L;
       }
     }
-    __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(HE_WARPS * 32, 4)
+    k_huff_encode(const uint8_t* __restrict__ in, unsigned long long n, uint32_t* rec_words, unsigned long long* lb,
+                  DevState* st) {
+  __shared__ unsigned long long stab[256];  // code | len << 56
+  __shared__ uint8_t slen[256];
+  __shared__ uint32_t wbuf[HE_WARPS][HE_BUF];
+  __shared__ uint32_t wpriv[HE_WARPS][HE_PRIV * 32];
+  __shared__ unsigned wx[HE_WARPS][HE_ROUNDS * 32];
+  const unsigned L = st->hf_len[threadIdx.x];
+  stab[threadIdx.x] = st->hf_code[threadIdx.x] | ((unsigned long long)L << 56);
+  slen[threadIdx.x] = (uint8_t)L;
+  for (int i = threadIdx.x; i < HE_WARPS * HE_BUF; i += blockDim.x) (&wbuf[0][0])[i] = 0;
+  const bool any_long = __syncthreads_or(L > 32);
+  uint32_t* buf = wbuf[threadIdx.x >> 5];
+  uint32_t* priv = wpriv[threadIdx.x >> 5];
+  he_tiles(in, n, rec_words, lb, stab, slen, buf, priv, wx[threadIdx.x >> 5], any_long);
 }
 
 void launch_huffman_encode(const uint8_t* seq, unsigned long long n, uint8_t* hf_rec, unsigned long long* lb_ws,
@@ -941,14 +1022,8 @@ void launch_huffman_encode(const uint8_t* seq, unsigned long long n, uint8_t* hf
   k_huff_zero<<<PERSIST_CTAS, 256, 0, s>>>(reinterpret_cast<uint32_t*>(hf_rec), st);
   (*launches)++;
   if (n == 0) return;
-  static const bool attr = [&] {  // once per process, thread-safe (C++11 static init)
-    cudaFuncSetAttribute(k_huff_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, HE_SMEM_WORDS * 4);
-    return true;
-  }();
-  (void)attr;
-  const unsigned long long tiles = cdiv(n, HE_TILE);
-  k_huff_encode<<<persist_grid(tiles), 256, HE_SMEM_WORDS * 4, s>>>(seq, n, reinterpret_cast<uint32_t*>(hf_rec),
-                                                                   lb_ws, st);
+  const unsigned long long tiles = cdiv(cdiv(n, HE_WTILE), HE_WARPS);
+  k_huff_encode<<<persist_grid(tiles), HE_WARPS * 32, 0, s>>>(seq, n, reinterpret_cast<uint32_t*>(hf_rec), lb_ws, st);
   (*launches)++;
 }
 

@@ -126,3 +126,28 @@ def test_fused_pipeline_decode_entry_points():
         tp = st.pipeline_tp_encode(data)
         assert st._decode(st._PIPE_CR, cr, len(data) + 64) == data
         assert st._decode(st._PIPE_TP, tp, len(data) + 64) == data
+
+
+def test_huffman_encode_tile_paths(oracle):
+    """Warp-tile encoder paths vs the oracle (stages.py:293-329): tiles denser
+    than 8 bits/symbol (global OR path), lanes whose 32 codes exceed 128 bits
+    (per-code shared-memory path), ragged tails, a single symbol."""
+    from paper_2507_11165_b200 import stages as st
+    rng = np.random.default_rng(17)
+    # near-uniform over 256 symbols: half the codes get 9 bits; sorting puts
+    # whole tiles of 9-bit symbols together
+    freq = np.where(np.arange(256) < 128, 1100, 900)
+    uni = np.repeat(np.arange(256, dtype=np.uint8), freq)
+    long_first = np.concatenate([uni[uni >= 128], uni[uni < 128]])
+    # Fibonacci-skewed: codes up to ~24 bits, rare symbols clustered per lane
+    fib = [1, 1]
+    while len(fib) < 26:
+        fib.append(fib[-1] + fib[-2])
+    skew = np.repeat(np.arange(26, dtype=np.uint8), fib[::-1])
+    cases = [long_first.tobytes(), rng.permutation(uni).tobytes(), skew.tobytes(),
+             rng.permutation(skew)[:77_777].tobytes(), bytes([7]) * 5000, b"\x01", b"\x02\x03" * 513,
+             rng.integers(0, 256, 1023).astype(np.uint8).tobytes()]
+    for i, data in enumerate(cases):
+        ref = oracle.stage_encode("huffman", data)
+        assert st.huffman_encode(data) == ref, i
+        assert st.huffman_decode(ref) == data, i
