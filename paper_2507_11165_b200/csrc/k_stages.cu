@@ -606,7 +606,11 @@ void launch_reduce_chain_impl(int stage, int width, int src_kind, const uint8_t*
   (*launches)++;
   static const bool split_tail = getenv("HB_SPLIT_TAIL") != nullptr;  // the four-launch form (variant tests)
   if (!split_tail) {
-    k_reduce_tail<<<PERSIST_CTAS, RD_THREADS, 0, s>>>(stage, width, bm, dev_ptr_tables, dev_ptr_tables + 4, lb_ws,
+    // sized by the level-1 input bound (level-0 bitmap: one bit per word):
+    // every CTA of the grid waits out each nested level, so small records
+    // must not pay for a full persistent grid
+    const unsigned gt = persist_grid(cdiv(cdiv(max_words, 8), RD_TILE));
+    k_reduce_tail<<<gt, RD_THREADS, 0, s>>>(stage, width, bm, dev_ptr_tables, dev_ptr_tables + 4, lb_ws,
                                                       lb_stride, rec_out, dst_off_dev, rec_len_dev);
     (*launches)++;
     return;
@@ -1082,8 +1086,8 @@ struct BmDec {
   unsigned long long orig[4], nsym[4], bm_off[4], bm_len[4], pay_off[4], pay_len[4];
 };
 
-__global__ void k_bm_parse(int stage, const uint8_t* rec, const unsigned long long* len_dev, BmDec* D,
-                           unsigned long long out_cap, unsigned long long* out_len, DevState* st) {
+__device__ void bm_parse(int stage, const uint8_t* rec, const unsigned long long* len_dev, BmDec* D,
+                         unsigned long long out_cap, unsigned long long* out_len, DevState* st) {
   D->ok = 0;
   if (st->flags & (F_STAGE | F_ARCHIVE)) return;
   unsigned long long off = 0, end = *len_dev;
@@ -1125,13 +1129,19 @@ __global__ void k_bm_parse(int stage, const uint8_t* rec, const unsigned long lo
   D->ok = 1;
 }
 
+__global__ void k_bm_parse(int stage, const uint8_t* rec, const unsigned long long* len_dev, BmDec* D,
+                           unsigned long long out_cap, unsigned long long* out_len, DevState* st) {
+  bm_parse(stage, rec, len_dev, D, out_cap, out_len, st);
+}
+
 // decode one level: bitmap bits + payload -> words (RRE: kept[cumsum-1], RZE: scatter).
 // STG / W: compile-time stage / width of the level (0 = runtime), one body
 // per combination the archives hold so each runs only its own width's code.
 template <int STG, int W>
 __device__ __forceinline__ void bm_decode_level(int stg_rt, int w_rt, unsigned long long nsym, const uint8_t* bm,
                                                 const uint8_t* pay, unsigned long long npay, uint8_t* out,
-                                                unsigned long long* lb, DevState* st) {
+                                                unsigned long long* lb, DevState* st,
+                                                unsigned long long* done = nullptr) {
   __shared__ unsigned long long sh[33];
   __shared__ unsigned long long tile_sh, base_sh;
   const int stg = STG ? STG : stg_rt;
@@ -1207,6 +1217,10 @@ __device__ __forceinline__ void bm_decode_level(int stg_rt, int w_rt, unsigned l
     }
     if (tile == ntiles - 1 && threadIdx.x == 0 && base_sh + total != npay) raise_flag(st, F_STAGE, 122);
     __syncthreads();
+    if (done && threadIdx.x == 0) {  // this tile's output is written (k_bm_decode_head waits on the count)
+      __threadfence();
+      atomicAdd(done, 1ull);
+    }
   }
 }
 
@@ -1234,13 +1248,60 @@ __global__ void __launch_bounds__(RD_THREADS)
     bm_decode_level<0, 0>(stg, w, nsym, bm, pay, npay, out, lb, st);
 }
 
+struct TmpPtrs {  // level k's decoded bitmap (k >= 1), by value
+  uint8_t* p[4];
+  __device__ uint8_t* operator[](int k) const { return p[k]; }
+};
+
+// The record header walk and the nested bitmap levels (3 -> 1, all small:
+// level k has 1/8^k of the level-0 symbols) in ONE launch: every CTA parses
+// the headers into shared memory (block 0 also publishes them for the
+// level-0 launch), then the CTAs take each level's tiles by ticket and wait
+// for the level's completion count before the next level reads its output.
+__global__ void __launch_bounds__(RD_THREADS)
+    k_bm_decode_head(int stage, const uint8_t* rec, const unsigned long long* len_dev, BmDec* Dg,
+                     unsigned long long out_cap, unsigned long long* out_len, TmpPtrs tmp,
+                     unsigned long long* lb_ws, unsigned long long lb_stride, DevState* st) {
+  __shared__ BmDec D;
+  __shared__ int go;
+  if (threadIdx.x == 0) {
+    unsigned long long dummy;
+    bm_parse(stage, rec, len_dev, &D, out_cap, blockIdx.x == 0 ? out_len : &dummy, st);
+    if (blockIdx.x == 0) *Dg = D;
+    go = D.ok;
+  }
+  __syncthreads();
+  if (!go) return;
+  for (int k = 3; k >= 1; k--) {
+    if (k > D.last) continue;
+    const int w = D.w[k];
+    const unsigned long long nsym = D.nsym[k];
+    const uint8_t* bm = k == D.last ? rec + D.bm_off[k] : tmp[k + 1];
+    const uint8_t* pay = rec + D.pay_off[k];
+    const unsigned long long npay = D.pay_len[k] / w;
+    if (nsym == 0) {
+      if (blockIdx.x == 0 && threadIdx.x == 0 && npay != 0) raise_flag(st, F_STAGE, 120);
+      continue;
+    }
+    unsigned long long* lb = lb_ws + (3 - k) * lb_stride;
+    unsigned long long* done = lb + lb_stride - 1;  // spare last entry of the level's zeroed region
+    if (w == 1)  // nested levels are RRE1 as written by the encoder
+      bm_decode_level<2, 1>(2, w, nsym, bm, pay, npay, tmp[k], lb, st, done);
+    else
+      bm_decode_level<0, 0>(2, w, nsym, bm, pay, npay, tmp[k], lb, st, done);
+    if (threadIdx.x == 0) {
+      const unsigned long long nt = cdiv(nsym, RD_TILE);
+      while (ld_acquire_u64(done) < nt) __nanosleep(64);
+    }
+    __syncthreads();
+  }
+}
+
 void launch_reduce_decode_impl(int stage, const uint8_t* rec, const unsigned long long* rec_len_dev,
                                unsigned long long out_cap, uint8_t* out, unsigned long long* out_len_dev,
                                uint8_t* const tmp[4], void* bmdec, unsigned long long* lb_ws,
                                unsigned long long lb_stride, DevState* st, cudaStream_t s, int* launches) {
   BmDec* D = reinterpret_cast<BmDec*>(bmdec);
-  k_bm_parse<<<1, 1, 0, s>>>(stage, rec, rec_len_dev, D, out_cap, out_len_dev, st);
-  (*launches)++;
   // innermost first: level k writes tmp[k] (k >= 1) or out (k == 0)
   unsigned long long words = out_cap;  // bound on level-0 symbols
   unsigned long long wb[4];
@@ -1248,6 +1309,19 @@ void launch_reduce_decode_impl(int stage, const uint8_t* rec, const unsigned lon
     wb[k] = words;
     words = cdiv(words, 8);
   }
+  static const bool split = getenv("HB_SPLIT_BM_DECODE") != nullptr;  // the five-launch form (variant tests)
+  if (!split) {
+    const TmpPtrs tp{{tmp[0], tmp[1], tmp[2], tmp[3]}};
+    k_bm_decode_head<<<persist_grid(cdiv(wb[1], RD_TILE)), RD_THREADS, 0, s>>>(stage, rec, rec_len_dev, D, out_cap,
+                                                                             out_len_dev, tp, lb_ws, lb_stride, st);
+    (*launches)++;
+    k_bm_decode<<<persist_grid(cdiv(wb[0], RD_TILE)), RD_THREADS, 0, s>>>(stage, 0, rec, D, tmp[1], out,
+                                                                        lb_ws + 3 * lb_stride, st);
+    (*launches)++;
+    return;
+  }
+  k_bm_parse<<<1, 1, 0, s>>>(stage, rec, rec_len_dev, D, out_cap, out_len_dev, st);
+  (*launches)++;
   for (int k = 3; k >= 0; k--) {
     const unsigned g = persist_grid(cdiv(wb[k], RD_TILE));
     k_bm_decode<<<g, RD_THREADS, 0, s>>>(stage, k, rec, D, k < 3 ? tmp[k + 1] : nullptr, k == 0 ? out : tmp[k],
@@ -1486,7 +1560,7 @@ constexpr unsigned HD_TCAP = 1u << 16;    // table rows (subsequences) per round
 __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsigned long long* len_dev,
                                                   unsigned long long n_expect, unsigned long long max_out,
                                                   unsigned long long nsub_cap, HDTables* T, DevState* st) {
-  __shared__ int ok_sh, cnt[257], maxlen_sh;
+  __shared__ int ok_sh, cnt[257], maxlen_sh, ns_sh;
   __shared__ uint8_t len[256];
   // shared copies of the canonical tables for the parallel LUT builds below
   __shared__ unsigned long long s_first[64];
@@ -1530,18 +1604,18 @@ __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsi
   if (!ok_sh) return;
   len[t] = rec[18 + t];
   cnt[t] = 0;
-  if (t == 0) cnt[256] = 0;
+  if (t == 0) cnt[256] = 0, ns_sh = 0;
+  if (t < 64) s_rank[t] = -1, s_count[t] = 0, s_first[t] = 0;
   __syncthreads();
   if (len[t]) {
     atomicAdd(&cnt[len[t]], 1);
     atomicMax(&maxlen_sh, (int)len[t]);
+    atomicAdd(&ns_sh, 1);
   }
   __syncthreads();
   const int maxlen = maxlen_sh;
   if (t == 0) {
-    int ns = 0;
-    for (int L = 1; L <= 255; L++) ns += cnt[L];
-    bool good = ns > 0;
+    bool good = ns_sh > 0;
     if (!good) raise_flag(st, F_STAGE, 156);
     long long avail = 1;
     for (int L = 1; L <= maxlen && good; L++) {  // Kraft, exact with a cap
@@ -1559,7 +1633,6 @@ __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsi
     if (good) {
       unsigned long long next = 0;
       int prev = 0, r = 0;
-      for (int L = 0; L < 64; L++) s_rank[L] = -1, s_count[L] = 0, s_first[L] = 0;
       for (int L = 1; L <= maxlen; L++) {
         if (!cnt[L]) continue;
         next <<= (L - prev);
@@ -1570,7 +1643,6 @@ __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsi
         next += cnt[L];
         r += cnt[L];
       }
-      for (int L = 0; L < 64; L++) T->first_rank[L] = s_rank[L], T->count[L] = s_count[L], T->first_code[L] = s_first[L];
       T->maxlen = maxlen;
       T->K = maxlen < HD_K ? maxlen : HD_K;
       unsigned S = HD_S_MAX;
@@ -1583,6 +1655,7 @@ __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsi
   }
   __syncthreads();
   if (!ok_sh) return;
+  if (t < 64) T->first_rank[t] = s_rank[t], T->count[t] = s_count[t], T->first_code[t] = s_first[t];
   // sorted symbol list: rank of symbol t among (len, sym)
   if (len[t]) {
     int r = 0;
@@ -1596,11 +1669,10 @@ __global__ void __launch_bounds__(256) k_hd_setup(const uint8_t* rec, const unsi
   for (int e = t; e < (1 << HD_K); e += 256) {
     uint16_t v = 0;
     if (e < (1 << K)) {
-      for (int L = 1; L <= K; L++) {
-        if (!s_count[L]) continue;
-        const unsigned long long c = (unsigned long long)e >> (K - L);
-        if (c >= s_first[L] && c - s_first[L] < (unsigned long long)s_count[L]) {
-          v = (uint16_t)((L << 8) | s_syms[s_rank[L] + (int)(c - s_first[L])]);
+      for (int L = 1; L <= K; L++) {  // codes of <= HD_K bits: 32-bit canonical test
+        const unsigned c = (unsigned)e >> (K - L), d = c - (unsigned)s_first[L];
+        if (d < (unsigned)s_count[L]) {
+          v = (uint16_t)((L << 8) | s_syms[s_rank[L] + (int)d]);
           break;
         }
       }

@@ -14,6 +14,8 @@ others so none of them ships untested:
                      instead of the seven per-class TMA passes
   HB_SPLIT_TAIL      reducer chain levels 1..3 and the record assembly as four
                      launches instead of the fused k_reduce_tail
+  HB_SPLIT_BM_DECODE bitmap decode as header parse + one launch per nested level
+                     instead of the fused k_bm_decode_head
 """
 import os
 import subprocess
@@ -38,6 +40,7 @@ VARIANTS = {
     "sweep": {"HB_SWEEP": "2"},
     "sweep-one": {"HB_SWEEP": "1"},
     "split-tail": {"HB_SPLIT_TAIL": "1"},
+    "split-bm-decode": {"HB_SPLIT_BM_DECODE": "1"},
 }
 
 
