@@ -151,3 +151,20 @@ def test_huffman_encode_tile_paths(oracle):
         ref = oracle.stage_encode("huffman", data)
         assert st.huffman_encode(data) == ref, i
         assert st.huffman_decode(ref) == data, i
+
+
+def test_huffman_codes_longer_than_32_bits(oracle):
+    """Fibonacci frequencies over 36 symbols give canonical codes of up to 35
+    bits: the encoder's per-code path for tables with codes > 32 bits and the
+    decoder's beyond-LUT path, against the oracle (stages.py:246-329)."""
+    from paper_2507_11165_b200 import stages as st
+    fib = [1, 1]
+    while len(fib) < 36:
+        fib.append(fib[-1] + fib[-2])
+    counts = fib[::-1]  # symbol 0 most frequent
+    data = np.repeat(np.arange(36, dtype=np.uint8), counts)
+    data = np.random.default_rng(9).permutation(data).tobytes()
+    ref = oracle.stage_encode("huffman", data)
+    assert max(ref[18:18 + 256]) >= 33  # some code is longer than 32 bits
+    assert st.huffman_encode(data) == ref
+    assert st.huffman_decode(ref) == data
