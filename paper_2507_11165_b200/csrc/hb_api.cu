@@ -456,6 +456,7 @@ __global__ void k_set_cfg_eb(DevState* st, uint8_t c0, uint8_t c1, uint8_t c2, u
   st->cfg[0] = c0, st->cfg[1] = c1, st->cfg[2] = c2, st->cfg[3] = c3;
   st->eb = eb;
   st->two_eb = __dmul_rn(2.0, eb);
+  st->inv_two_eb = __ddiv_rn(1.0, st->two_eb);
 }
 __global__ void k_check_len(const unsigned long long* len, unsigned long long want, DevState* st, uint32_t flag) {
   if (!(st->flags & (F_STAGE | F_ARCHIVE)) && *len != want) raise_flag(st, flag, 200);

@@ -72,6 +72,7 @@ struct DevState {
   int hd_maxlen;
   unsigned long long tickets[16];
   unsigned long long scratch[32];
+  double inv_two_eb;  // __ddiv_rn(1.0, two_eb), set with eb (one IEEE division per call, not per block)
 };
 
 __device__ __forceinline__ void raise_flag(DevState* st, uint32_t f, uint32_t detail = 0) {

@@ -396,7 +396,7 @@ template <bool DEC>
 __device__ __forceinline__ void sweep_consts(const TPassArgs& A) {
   sh_eb[0] = A.st->eb;
   sh_eb[1] = A.st->two_eb;
-  sh_eb[2] = __ddiv_rn(1.0, sh_eb[1]);
+  sh_eb[2] = A.st->inv_two_eb;
   sh_ocount = DEC ? *A.ocount : 0;
 }
 
@@ -425,7 +425,7 @@ __device__ __forceinline__ bool tp_block(const TPassArgs& A, const TMaps& M, int
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       s_eb[0] = A.st->eb;
       s_eb[1] = A.st->two_eb;
-      s_eb[2] = __ddiv_rn(1.0, s_eb[1]);  // one IEEE division per block
+      s_eb[2] = A.st->inv_two_eb;  // __ddiv_rn(1.0, two_eb), computed once with eb
       s_ocount = DEC ? *A.ocount : 0;
     }
     if (!DEC)

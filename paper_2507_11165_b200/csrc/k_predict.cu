@@ -167,6 +167,7 @@ __global__ void k_finish_eb(DevState* st, int eb_mode, double mag) {
   if (!(isfinite(eb) && eb > 0)) raise_flag(st, F_DEGENERATE, 2);
   st->eb = eb;
   st->two_eb = __dmul_rn(2.0, eb);
+  st->inv_two_eb = __ddiv_rn(1.0, st->two_eb);
 }
 
 __global__ void k_minmax_init(DevState* st) {
@@ -198,6 +199,7 @@ __global__ void k_set_eb(DevState* st, double eb) {
   if (!(isfinite(eb) && eb > 0)) raise_flag(st, F_DEGENERATE, 2);
   st->eb = eb;
   st->two_eb = __dmul_rn(2.0, eb);
+  st->inv_two_eb = __ddiv_rn(1.0, st->two_eb);
 }
 
 void launch_set_eb(DevState* st, double eb, cudaStream_t s, int* launches) {
