@@ -895,7 +895,8 @@ __device__ __forceinline__ unsigned he_pack_lane(const uint32_t (&w)[8], int cnt
 __device__ __forceinline__ void he_tiles(const uint8_t* __restrict__ in, unsigned long long n, uint32_t* rec_words,
                                          unsigned long long* lb, const unsigned long long* stab,
                                          const uint8_t* slen, uint32_t* buf, uint32_t* priv, unsigned* sx,
-                                         bool long_codes) {
+                                         bool long_codes, int zsym, unsigned zlen) {
+  const uint32_t zrep = 0x01010101u * (uint32_t)(zsym & 0xFF);
   const int lane = threadIdx.x & 31;
   unsigned long long* status = lb + 1;
   const unsigned long long ntiles = cdiv(n, HE_WTILE);
@@ -943,6 +944,41 @@ __device__ __forceinline__ void he_tiles(const uint8_t* __restrict__ in, unsigne
       bool fits;
       const unsigned e0 = sx[r * 32 + lane];
       unsigned nb = 0;
+      if (zsym >= 0) {
+        // sparse: only codes with a set bit are written; the all-zero code
+        // (the most frequent symbol of a skewed histogram) only advances the
+        // position.  Mask of the lane's other symbols, SWAR per 4 bytes
+        uint32_t nz = 0;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const uint32_t b = ~__vcmpeq4(w[q], zrep) & 0x80808080u;  // byte MSB set = not the zero-code symbol
+          nz |= ((b * 0x00204081u) >> 28) << (4 * q);                // bits 7/15/23/31 -> bits 0..3
+          priv[lane + 32 * q] = w[q];                                  // lane bytes for indexed access
+        }
+        if (cnt < HE_SYMS) nz &= (1u << cnt) - 1u;
+        const uint8_t* pb = reinterpret_cast<const uint8_t*>(priv);
+        unsigned pos = e0;
+        int prev = -1;
+        while (nz) {
+          const int k = __ffs(nz) - 1;
+          nz &= nz - 1;
+          pos += (unsigned)(k - prev - 1) * zlen;
+          prev = k;
+          const unsigned long long e = stab[pb[4 * (lane + 32 * (k >> 2)) + (k & 3)]];
+          const int L = (int)(e >> 56);
+          if (L <= 32) {
+            const uint64_t v = (e & 0xFFFFFFFFull) << (64 - (int)(pos & 31) - L);
+            const unsigned wi = pos >> 5;
+            if ((uint32_t)(v >> 32)) atomicOr(&buf[wi], (uint32_t)(v >> 32));
+            if ((uint32_t)v) atomicOr(&buf[wi + 1], (uint32_t)v);
+          } else {
+            he_put<false>(buf, pos, L, e & ((1ull << 56) - 1));
+          }
+          pos += (unsigned)L;
+        }
+        __syncwarp();  // private words reused by the next round
+        continue;
+      }
       if (long_codes)
         fits = false;
       else if (cnt == HE_SYMS)
@@ -1015,10 +1051,19 @@ __global__ void __launch_bounds__(HE_WARPS * 32, 4)
   stab[threadIdx.x] = st->hf_code[threadIdx.x] | ((unsigned long long)L << 56);
   slen[threadIdx.x] = (uint8_t)L;
   for (int i = threadIdx.x; i < HE_WARPS * HE_BUF; i += blockDim.x) (&wbuf[0][0])[i] = 0;
+  __shared__ int zsym_sh;
+  if (threadIdx.x == 0) zsym_sh = -1;
+  __syncthreads();
+  // the canonical all-zero code (unique): the sparse pack pays off when that
+  // symbol is a large share of the stream (smooth fields), not on flat
+  // histograms (rough fields), where the bit-writer pack is kept
+  if (L && st->hf_code[threadIdx.x] == 0 && st->hist[threadIdx.x] * 4 >= n) zsym_sh = (int)threadIdx.x;
   const bool any_long = __syncthreads_or(L > 32);
+  const int zsym = zsym_sh;
   uint32_t* buf = wbuf[threadIdx.x >> 5];
   uint32_t* priv = wpriv[threadIdx.x >> 5];
-  he_tiles(in, n, rec_words, lb, stab, slen, buf, priv, wx[threadIdx.x >> 5], any_long);
+  he_tiles(in, n, rec_words, lb, stab, slen, buf, priv, wx[threadIdx.x >> 5], any_long, zsym,
+           zsym >= 0 ? slen[zsym] : 0u);
 }
 
 void launch_huffman_encode(const uint8_t* seq, unsigned long long n, uint8_t* hf_rec, unsigned long long* lb_ws,
